@@ -1,0 +1,354 @@
+// mg_api.cu — the extern "C" boundary declared in include/modal_b200.h.
+//
+// Every entry point: validate arguments, select the device, run, and translate failures
+// into MG_E* codes with a thread-local message (mg_last_error).  No CPU fallback exists:
+// without an sm_100 device the compute entry points return MG_ECUDA.
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "mg_common.cuh"
+#include "mg_domain.cuh"
+#include "mg_gamma.cuh"
+
+namespace mg {
+void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x, int Nx,
+                      const double* eps, const double* qk, int p, int l_min, int l_max,
+                      double X, double kd, double amp, double* C_dev, double* qt_dev,
+                      double* delta_out_dev, cudaStream_t s);
+void bessel_table(const double* z, int nz, int l_max, double* out);
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+DeviceGuard::DeviceGuard(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        fail(MG_ECUDA, "no CUDA device available (the Γ library has no CPU fallback)");
+    }
+    MG_REQUIRE(device >= 0 && device < n, "device index out of range");
+    MG_CUDA(cudaGetDevice(&prev));
+    MG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    MG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) fail(MG_ECUDA, "library is built for sm_100a (B200) only");
+}
+}  // namespace mg
+
+using namespace mg;
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return MG_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host out of memory";
+        return MG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return MG_ECUDA;
+    }
+}
+
+static void full_range_bounds(const DomainIndex& D, int64_t begin, int64_t end, int* s, int* e) {
+    MG_REQUIRE(0 <= begin && begin <= end && end <= D.count, "invalid flat range");
+    D.triple(begin, s[0], s[1], s[2]);
+    D.triple(end, e[0], e[1], e[2]);
+}
+
+extern "C" {
+
+int mg_version(void) { return 100; }
+
+const char* mg_last_error(void) { return g_last_error.c_str(); }
+
+int mg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int mg_domain_count(int l_min, int l_max, int64_t* count, int64_t* rows) {
+    return guarded([&] {
+        MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
+        int64_t c = 0, r = 0;
+        for (int l1 = l_min; l1 <= l_max; ++l1)
+            for (int l2 = l1; l2 <= l_max; ++l2) {
+                int n = row_len(l1, l2, l_max);
+                c += n;
+                r += n > 0;
+            }
+        if (count) *count = c;
+        if (rows) *rows = r;
+    });
+}
+
+int mg_domain_triples(int l_min, int l_max, int64_t begin, int64_t end, int32_t* l1,
+                      int32_t* l2, int32_t* l3, int device) {
+    return guarded([&] {
+        MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
+        MG_REQUIRE(l1 && l2 && l3, "null output");
+        DeviceGuard g(device);
+        weights(l_min, l_max, nullptr, nullptr, 0, begin, end, nullptr, l1, l2, l3);
+    });
+}
+
+int mg_weights(int l_min, int l_max, const double* C, const double* v, int h2_mode,
+               int64_t begin, int64_t end, double* zm, int device) {
+    return guarded([&] {
+        MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
+        MG_REQUIRE(C && v && zm, "null argument");
+        MG_REQUIRE(h2_mode == MG_H2_GOSPER || h2_mode == MG_H2_EXACT, "unknown h2_mode");
+        DeviceGuard g(device);
+        weights(l_min, l_max, C, v, h2_mode, begin, end, zm, nullptr, nullptr, nullptr);
+    });
+}
+
+int mg_plan_create(const double* q, const double* qt, const double* C, const double* v,
+                   const double* wr2, const int64_t* modes, int p, int Nx, int n, int l_min,
+                   int l_max, int h2_mode, int device, mg_plan** plan) {
+    return guarded([&] {
+        MG_REQUIRE(q && qt && C && v && wr2 && modes && plan, "null argument");
+        DeviceGuard g(device);
+        auto* P = new mg_plan();
+        try {
+            P->device = device;
+            plan_init(P, q, qt, nullptr, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode);
+        } catch (...) {
+            delete P;
+            throw;
+        }
+        *plan = P;
+    });
+}
+
+int mg_plan_create_dev(const double* q, const double* qt_dev, const double* C,
+                       const double* v, const double* wr2, const int64_t* modes, int p,
+                       int Nx, int n, int l_min, int l_max, int h2_mode, int device,
+                       mg_plan** plan) {
+    return guarded([&] {
+        MG_REQUIRE(q && qt_dev && C && v && wr2 && modes && plan, "null argument");
+        DeviceGuard g(device);
+        auto* P = new mg_plan();
+        try {
+            P->device = device;
+            plan_init(P, q, nullptr, qt_dev, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode);
+        } catch (...) {
+            delete P;
+            throw;
+        }
+        *plan = P;
+    });
+}
+
+int mg_plan_execute(mg_plan* P, int l2_begin, int l2_end, double* gamma_dev, void* stream) {
+    return guarded([&] {
+        MG_REQUIRE(P, "null plan");
+        DeviceGuard g(P->device);
+        if (l2_end < 0) l2_end = P->l_max + 1;
+        int s[3] = {P->l_min, 0, 0}, e[3] = {P->l_max + 1, 0, 0};
+        std::vector<MgRow> rows;
+        build_rows(P, l2_begin, l2_end, s, e, rows);
+        cudaStream_t st = (cudaStream_t)stream;
+        execute_rows(P, rows, st);
+        if (gamma_dev)
+            MG_CUDA(cudaMemcpyAsync(gamma_dev, P->gamma.p, (size_t)P->nm * P->nm * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, st));
+    });
+}
+
+int mg_plan_fetch(mg_plan* P, double* gamma, void* stream) {
+    return guarded([&] {
+        MG_REQUIRE(P && gamma, "null argument");
+        DeviceGuard g(P->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        MG_CUDA(cudaMemcpyAsync(gamma, P->gamma.p, (size_t)P->nm * P->nm * sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+        MG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int mg_plan_stats(mg_plan* P, double* f_run, double* f_x, double* f_pair, int64_t* launches) {
+    return guarded([&] {
+        MG_REQUIRE(P, "null plan");
+        if (f_run) *f_run = P->flops_run;
+        if (f_x) *f_x = P->flops_x;
+        if (f_pair) *f_pair = P->flops_pair;
+        if (launches) *launches = P->launches;
+    });
+}
+
+void mg_plan_destroy(mg_plan* P) {
+    if (!P) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(P->device);
+    delete P;
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+static void gamma_common(const double* q, const double* qt, const double* C, const double* v,
+                         const double* wr2, const int64_t* modes, int p, int Nx, int n,
+                         int l_min, int l_max, int h2_mode, int device, double* gamma,
+                         const std::function<void(mg_plan*)>& run) {
+    MG_REQUIRE(q && qt && C && v && wr2 && modes && gamma, "null argument");
+    DeviceGuard g(device);
+    mg_plan P;
+    P.device = device;
+    plan_init(&P, q, qt, nullptr, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode);
+    run(&P);
+    MG_CUDA(cudaMemcpy(gamma, P.gamma.p, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+int mg_gamma_sep(const double* q, const double* qt, const double* C, const double* v,
+                 const double* wr2, const int64_t* modes, int p, int Nx, int n, int l_min,
+                 int l_max, int h2_mode, int64_t begin, int64_t end, int device,
+                 double* gamma) {
+    return guarded([&] {
+        gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, device, gamma,
+                     [&](mg_plan* P) {
+                         DomainIndex D;
+                         D.build(l_min, l_max);
+                         int64_t e_ = end < 0 ? D.count : end;
+                         int s[3], e[3];
+                         full_range_bounds(D, begin, e_, s, e);
+                         std::vector<MgRow> rows;
+                         if (begin < e_) build_rows(P, l_min, l_max + 1, s, e, rows);
+                         execute_rows(P, rows, 0);
+                     });
+    });
+}
+
+int mg_gamma_sep_slab(const double* q, const double* qt, const double* C, const double* v,
+                      const double* wr2, const int64_t* modes, int p, int Nx, int n,
+                      int l_min, int l_max, int h2_mode, int l2_begin, int l2_end,
+                      int device, double* gamma) {
+    return guarded([&] {
+        gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, device, gamma,
+                     [&](mg_plan* P) {
+                         int s[3] = {l_min, 0, 0}, e[3] = {l_max + 1, 0, 0};
+                         std::vector<MgRow> rows;
+                         build_rows(P, l2_begin, l2_end < 0 ? l_max + 1 : l2_end, s, e, rows);
+                         execute_rows(P, rows, 0);
+                     });
+    });
+}
+
+int mg_gamma_sep_triples(const double* q, const double* qt, const double* C,
+                         const double* v, const double* wr2, const int64_t* modes, int p,
+                         int Nx, int n, int l_min, int l_max, int h2_mode,
+                         const int32_t* l1, const int32_t* l2, const int32_t* l3,
+                         int64_t count, int device, double* gamma) {
+    return guarded([&] {
+        MG_REQUIRE(count == 0 || (l1 && l2 && l3), "null triple arrays");
+        gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, device, gamma,
+                     [&](mg_plan* P) { execute_triples(P, l1, l2, l3, count, 0); });
+    });
+}
+
+int mg_slab_plan(int l_min, int l_max, int p, int Nx, int nshards, int* bounds) {
+    return guarded([&] {
+        MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
+        MG_REQUIRE(nshards >= 1 && bounds, "invalid shard count");
+        const double pairs = p * (p + 1) / 2.0;
+        std::vector<double> cum(l_max - l_min + 2, 0.0);
+        for (int l2 = l_min; l2 <= l_max; ++l2) {
+            double c = 0;
+            for (int l3 = l2; l3 <= std::min(2 * l2, l_max); ++l3) {
+                int par = (l2 + l3) & 1;
+                int lo = std::max(l_min, l3 - l2);
+                if ((lo & 1) != par) ++lo;
+                int hi = (l2 & 1) == par ? l2 : l2 - 1;
+                if (lo > hi) continue;
+                double m = (hi - lo) / 2 + 1;
+                c += (double)p * p * Nx * m + pairs * p * p * Nx;
+            }
+            cum[l2 - l_min + 1] = cum[l2 - l_min] + c;
+        }
+        bounds[0] = l_min;
+        for (int s = 1; s < nshards; ++s) {
+            double target = cum.back() * s / nshards;
+            int idx = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+            bounds[s] = std::max(bounds[s - 1], std::min(l_min + idx, l_max + 1));
+        }
+        bounds[nshards] = l_max + 1;
+    });
+}
+
+int mg_build_qtilde(const double* k, const double* wk, int Nk, const double* x, int Nx,
+                    const double* eps, const double* qk, int p, int l_min, int l_max,
+                    double x_delta, double k_damp, double eps_amp, int device, double* C,
+                    double* qt, double* delta) {
+    return guarded([&] {
+        MG_REQUIRE(k && wk && x && eps && qk, "null argument");
+        DeviceGuard g(device);
+        const int L = l_max - l_min + 1;
+        DBuf<double> dC, dqt, dd;
+        if (C) dC.alloc(L);
+        if (qt) dqt.alloc((size_t)p * Nx * L);
+        if (delta) dd.alloc((size_t)L * Nk);
+        build_qtilde_dev(k, wk, Nk, x, Nx, eps, qk, p, l_min, l_max, x_delta, k_damp, eps_amp,
+                         dC.p, dqt.p, dd.p, 0);
+        if (C) MG_CUDA(cudaMemcpy(C, dC.p, L * sizeof(double), cudaMemcpyDeviceToHost));
+        if (qt)
+            MG_CUDA(cudaMemcpy(qt, dqt.p, (size_t)p * Nx * L * sizeof(double),
+                               cudaMemcpyDeviceToHost));
+        if (delta)
+            MG_CUDA(cudaMemcpy(delta, dd.p, (size_t)L * Nk * sizeof(double),
+                               cudaMemcpyDeviceToHost));
+    });
+}
+
+int mg_build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x, int Nx,
+                        const double* eps, const double* qk, int p, int l_min, int l_max,
+                        double x_delta, double k_damp, double eps_amp, int device,
+                        double* C_dev, double* qt_dev, void* stream) {
+    return guarded([&] {
+        MG_REQUIRE(k && wk && x && eps && qk, "null argument");
+        DeviceGuard g(device);
+        build_qtilde_dev(k, wk, Nk, x, Nx, eps, qk, p, l_min, l_max, x_delta, k_damp, eps_amp,
+                         C_dev, qt_dev, nullptr, (cudaStream_t)stream);
+    });
+}
+
+int mg_bessel_table(const double* z, int nz, int l_max, int device, double* out) {
+    return guarded([&] {
+        MG_REQUIRE(z && out, "null argument");
+        DeviceGuard g(device);
+        bessel_table(z, nz, l_max, out);
+    });
+}
+
+int mg_gamma_nonsep(const double* q, const double* qt, const double* C, const double* v,
+                    const double* wr2, const int64_t* modes, int p, int Nx, int n, int l_min,
+                    int l_max, int h2_mode, const double* alpha, const int32_t* l1,
+                    const int32_t* l2, const int32_t* l3, const double* W, int64_t count,
+                    int device, double* b) {
+    return guarded([&] {
+        MG_REQUIRE(q && qt && C && v && wr2 && modes && alpha && b, "null argument");
+        MG_REQUIRE(count == 0 || (l1 && l2 && l3 && W), "null triple arrays");
+        DeviceGuard g(device);
+        mg_plan P;
+        P.device = device;
+        plan_init(&P, q, qt, nullptr, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode);
+        if (count == 0) {
+            std::memset(b, 0, sizeof(double) * n);
+            return;
+        }
+        nonsep(&P, alpha, l1, l2, l3, W, count, b, 0);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,862 @@
+// mg_gamma.cu — separable Γ on the tetrahedral domain, row-factorised onto DMMA GEMMs.
+//
+// Reference: engine3d.py:86-136 (_block_accumulate / _sweep_chunk): per triple t,
+//   P[n,t]  = Σ_6perms q q q,  X[n',t] = zm_t Σ_x wr2_x Σ_6perms q̃ q̃ q̃,  Γ += P Xᵀ.
+// The reference spends 96-98% of its time building X (engine3d.py:115-116).
+//
+// B200 formulation.  Single out l1 (the smallest multipole) and group the
+// ordered triples into (l2,l3)-rows; l1 runs over a parity class window of the row.  With
+// pair sums Sq_ab = q_a(l2)q_b(l3) + q_b(l2)q_a(l3), S_ab(x) = q̃_a(x,l2)q̃_b(x,l3) + (a<->b):
+//   P[(ijk),t]     = q_k(l1) Sq_ij + q_j(l1) Sq_ik + q_i(l1) Sq_jk
+//   f[(i'j'k'),x,t] = q̃_k'(x,l1) S_i'j'(x) + q̃_j'(x,l1) S_i'k'(x) + q̃_i'(x,l1) S_j'k'(x)
+// so, contracting the l1-run first and x second,
+//   H_row[c,c',x]   = Σ_{l1} zm(l1,l2,l3) q_c(l1) wr2_x q̃_c'(x,l1)        (K1, GEMM over l1)
+//   G_row[ab',c,c'] = Σ_x S_ab'(x) H_row[c,c',x]                           (K2, GEMM over x)
+//   Z[ab,c,n']     += Σ_rows Sq_ab(row) Σ_{(a'b',c'') ∈ dec(n')} G_row[a'b',c,c'']  (K3, GEMM over rows)
+//   Γ[(ijk),n']     = Z[ij,k,n'] + Z[ik,j,n'] + Z[jk,i,n']                   (final gather)
+// All three contractions are FP64 DMMA block GEMMs (mg_dmma.cuh) whose operand loaders
+// generate the pair products / weights / gathers on the fly.  No atomics: every output tile
+// is owned by exactly one CTA per launch and rows are reduced in a fixed order, so a run is
+// bitwise reproducible.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "mg_dmma.cuh"
+#include "mg_gamma.cuh"
+
+namespace mg {
+
+// ------------------------------------------------------------------------------------------
+// setup kernels
+// ------------------------------------------------------------------------------------------
+
+// QT[l][c][x] = q̃[c][x][l] ; WQT[cls(l)][c][x] = wr2[x] q̃[c][x][l]  (x zero-padded to NxP)
+__global__ void k_transpose_qt(const double* __restrict__ qt, const double* __restrict__ wr2,
+                               int p, int Nx, int NxP, int L, int l_min, int l0_1, int n0,
+                               double* __restrict__ QT, double* __restrict__ WQT) {
+    int64_t total = (int64_t)L * p * NxP;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int x = (int)(i % NxP);
+        int64_t r = i / NxP;
+        int c = (int)(r % p);
+        int li = (int)(r / p);
+        double val = x < Nx ? qt[((int64_t)c * Nx + x) * L + li] : 0.0;
+        QT[i] = val;
+        int l = l_min + li;
+        int s = ((l ^ l_min) & 1) == 0 ? (l - l_min) / 2 : n0 + (l - l0_1) / 2;
+        WQT[((int64_t)s * p + c) * NxP + x] = x < Nx ? wr2[x] * val : 0.0;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K0: per-row weight windows  ZT[off(row) + j - jlo] = zm(l1(j), l2, l3)
+// ------------------------------------------------------------------------------------------
+__global__ void k_row_weights(const MgRow* __restrict__ rows, const int64_t* __restrict__ zoff,
+                              int64_t zbase, int l_min, const int* __restrict__ l0,
+                              const double* __restrict__ C, const double* __restrict__ v,
+                              const double* __restrict__ lf, int mode,
+                              double* __restrict__ ZT) {
+    MgRow r = rows[blockIdx.x];
+    int64_t o = zoff[blockIdx.x] - zbase;
+    for (int j = r.jlo + threadIdx.x; j <= r.jhi; j += blockDim.x) {
+        int l1 = l0[r.par] + 2 * j;
+        ZT[o + j - r.jlo] = zm_weight(mode, l1, r.l2, r.l3, C, v, l_min, lf);
+    }
+}
+
+// explicit-triple variant: ZT pre-zeroed, then zm of listed triples scattered (x count)
+__global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
+                                  const int32_t* __restrict__ t3, const int64_t* __restrict__ pos,
+                                  const double* __restrict__ dup, int64_t n, int64_t zbase,
+                                  int l_min, const double* __restrict__ C,
+                                  const double* __restrict__ v, const double* __restrict__ lf,
+                                  int mode, double* __restrict__ ZT) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        ZT[pos[i] - zbase] = dup[i] * zm_weight(mode, t1[i], t2[i], t3[i], C, v, l_min, lf);
+}
+
+// ------------------------------------------------------------------------------------------
+// K1: run contraction  H[(r,c)][(c',x)] = Σ_j A[(r,c)][j] WQT[cls+j][(c',x)]
+// ------------------------------------------------------------------------------------------
+struct RunA {  // A[slot][j] = ZT * q[c][l1], k-run map
+    const double* zt;   // row's ZT window base (valid if ok)
+    const double* qc;   // q[c][*] shifted so that qc[l1] is q_c(l1)
+    int jlo, jhi, jt0, l0;
+    bool ok;
+    __device__ void load(int kt, Frag8& r) const {
+        int k0 = (threadIdx.x >> 7) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            int j = jt0 + kt * GB_K + k0 + i;
+            bool in = ok && j >= jlo && j <= jhi;
+            r.v[i] = in ? zt[j - jlo] * qc[l0 + 2 * j] : 0.0;
+        }
+    }
+    __device__ void store(double* S, const Frag8& r) const { store_krun(S, GB_LDA, r); }
+};
+struct RunB {  // B[j][n] = WQT[cls+j][n], m-run map, n contiguous
+    const double* base;  // WQT + cls*ldb
+    int64_t ldb;         // p * NxP
+    int jt0, jhi, n0;
+    __device__ void load(int kt, Frag8& r) const {
+        int k = threadIdx.x >> 4, n = n0 + (threadIdx.x & 15) * 8;
+        int j = jt0 + kt * GB_K + k;
+        if (j <= jhi && n < ldb) {
+            const double2* s = reinterpret_cast<const double2*>(base + (int64_t)j * ldb + n);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double2 d = __ldg(s + i);
+                r.v[2 * i] = d.x;
+                r.v[2 * i + 1] = d.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r.v[i] = 0.0;
+        }
+    }
+    __device__ void store(double* S, const Frag8& r) const { store_mrun(S, GB_LDB, r); }
+};
+
+__global__ void __launch_bounds__(GB_THREADS, 1)
+k_run_contract(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
+               const int64_t* __restrict__ zoff, int64_t zbase, int row_base,
+               const double* __restrict__ ZT, const double* __restrict__ q,
+               const double* __restrict__ WQT, int p, int P8, int NxP, int L, int l_min,
+               int l0e, int l0o, int cbase0, int cbase1, double* __restrict__ H) {
+    extern __shared__ __align__(16) double smem[];
+    const MgTile tl = tiles[blockIdx.y];
+    const int n0 = blockIdx.x * GB_N;
+    const int64_t ldb = (int64_t)p * NxP;
+    const MgRow r0 = rows[tl.row0];
+    const int par = r0.par;
+    const int l0 = par ? l0o : l0e;
+    RunA la;
+    {
+        int m = threadIdx.x & 127;
+        int rr = m / P8, c = m - rr * P8;
+        la.ok = rr < tl.nrows && c < p;
+        MgRow rw = la.ok ? rows[tl.row0 + rr] : r0;
+        la.zt = ZT + (zoff[tl.row0 + (la.ok ? rr : 0)] - zbase);
+        la.qc = q + (int64_t)(la.ok ? c : 0) * L - l_min;
+        la.jlo = rw.jlo;
+        la.jhi = rw.jhi;
+        la.jt0 = tl.jlo;
+        la.l0 = l0;
+    }
+    RunB lb;
+    lb.base = WQT + (int64_t)(par ? cbase1 : cbase0) * ldb;
+    lb.ldb = ldb;
+    lb.jt0 = tl.jlo;
+    lb.jhi = tl.jhi;
+    lb.n0 = n0;
+    Acc acc;
+    gemm_mainloop((tl.jhi - tl.jlo + GB_K) / GB_K, la, lb, smem, acc);
+    acc_foreach_pair(acc, [&](int m, int n, double v0, double v1) {
+        int rr = m / P8, c = m - rr * P8;
+        int gn = n0 + n;
+        if (rr < tl.nrows && c < p && gn < ldb) {
+            int64_t hr = (int64_t)(tl.row0 + rr - row_base) * p + c;
+            *reinterpret_cast<double2*>(H + hr * ldb + gn) = make_double2(v0, v1);
+        }
+    });
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: x contraction  G[r][ab][(c,c')] = Σ_x S_ab(x) H[r][(c,c')][x]
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void pair_of(int pr, int& a, int& b) {
+    int bb = (int)((sqrt(8.0 * pr + 1.0) - 1.0) * 0.5);
+    while ((bb + 1) * (bb + 2) / 2 <= pr) ++bb;
+    while (bb * (bb + 1) / 2 > pr) --bb;
+    b = bb;
+    a = pr - bb * (bb + 1) / 2;
+}
+__device__ __forceinline__ int pair_idx(int a, int b) {  // a <= b
+    return b * (b + 1) / 2 + a;
+}
+
+struct XA {  // S[pair][x], k-run map
+    const double *r2a, *r2b, *r3a, *r3b;
+    bool ok;
+    __device__ void load(int kt, Frag8& r) const {
+        int x0 = kt * GB_K + (threadIdx.x >> 7) * 8;
+        if (ok) {
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+                double2 a2 = *reinterpret_cast<const double2*>(r2a + x0 + i);
+                double2 b2 = *reinterpret_cast<const double2*>(r2b + x0 + i);
+                double2 a3 = *reinterpret_cast<const double2*>(r3a + x0 + i);
+                double2 b3 = *reinterpret_cast<const double2*>(r3b + x0 + i);
+                r.v[i] = a2.x * b3.x + b2.x * a3.x;
+                r.v[i + 1] = a2.y * b3.y + b2.y * a3.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r.v[i] = 0.0;
+        }
+    }
+    __device__ void store(double* S, const Frag8& r) const { store_krun(S, GB_LDA, r); }
+};
+struct XB {  // H[r][cc'][x], k-run map
+    const double* h;
+    bool ok;
+    __device__ void load(int kt, Frag8& r) const {
+        int x0 = kt * GB_K + (threadIdx.x >> 7) * 8;
+        if (ok) {
+            const double2* s = reinterpret_cast<const double2*>(h + x0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double2 d = s[i];
+                r.v[2 * i] = d.x;
+                r.v[2 * i + 1] = d.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r.v[i] = 0.0;
+        }
+    }
+    __device__ void store(double* S, const Frag8& r) const { store_krun(S, GB_LDB, r); }
+};
+
+__global__ void __launch_bounds__(GB_THREADS, 1)
+k_x_contract(const MgRow* __restrict__ rows, int row_b1, int row_b3,
+             const double* __restrict__ QT, const double* __restrict__ H, int p, int P2,
+             int NxP, int l_min, double* __restrict__ G) {
+    extern __shared__ __align__(16) double smem[];
+    const int r = blockIdx.z;  // row within the K1/K2 batch
+    const MgRow rw = rows[row_b1 + r];
+    const int m0 = blockIdx.y * GB_M, n0 = blockIdx.x * GB_N;
+    const int pp = p * p;
+    XA la;
+    {
+        int pr = m0 + (threadIdx.x & 127);
+        la.ok = pr < P2;
+        int a = 0, b = 0;
+        if (la.ok) pair_of(pr, a, b);
+        const double* q2 = QT + (int64_t)(rw.l2 - l_min) * p * NxP;
+        const double* q3 = QT + (int64_t)(rw.l3 - l_min) * p * NxP;
+        la.r2a = q2 + (int64_t)a * NxP;
+        la.r2b = q2 + (int64_t)b * NxP;
+        la.r3a = q3 + (int64_t)a * NxP;
+        la.r3b = q3 + (int64_t)b * NxP;
+    }
+    XB lb;
+    {
+        int cc = n0 + (threadIdx.x & 127);
+        lb.ok = cc < pp;
+        lb.h = H + ((int64_t)r * pp + (lb.ok ? cc : 0)) * NxP;
+    }
+    Acc acc;
+    gemm_mainloop(NxP / GB_K, la, lb, smem, acc);
+    double* Gr = G + (int64_t)(row_b1 + r - row_b3) * P2 * pp;
+    acc_foreach_pair(acc, [&](int m, int n, double v0, double v1) {
+        int pr = m0 + m, cc = n0 + n;
+        if (pr < P2) {
+            if (cc < pp) Gr[(int64_t)pr * pp + cc] = v0;
+            if (cc + 1 < pp) Gr[(int64_t)pr * pp + cc + 1] = v1;
+        }
+    });
+}
+
+// ------------------------------------------------------------------------------------------
+// K3: pair contraction over rows  Z[ab][(c,n')] += Σ_r Sq_ab(r) R_r[c][n']
+// ------------------------------------------------------------------------------------------
+struct PA {  // Sq[pair][row], k-run map
+    const MgRow* rows;
+    const double *qa, *qb;  // q[a][*], q[b][*] shifted by -l_min
+    int nrows;
+    bool ok;
+    __device__ void load(int kt, Frag8& r) const {
+        int k0 = kt * GB_K + (threadIdx.x >> 7) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            int rr = k0 + i;
+            if (ok && rr < nrows) {
+                MgRow w = rows[rr];
+                r.v[i] = qa[w.l2] * qb[w.l3] + qb[w.l2] * qa[w.l3];
+            } else {
+                r.v[i] = 0.0;
+            }
+        }
+    }
+    __device__ void store(double* S, const Frag8& r) const { store_krun(S, GB_LDA, r); }
+};
+struct PB {  // R[row][n] gathered from G, m-run map
+    const double* G;
+    const int* modes;
+    int p, P2, nm, nrows, ncols, n0;
+    __device__ void load(int kt, Frag8& r) const {
+        int rr = kt * GB_K + (threadIdx.x >> 4);
+        int nb = n0 + (threadIdx.x & 15) * 8;
+        const int pp = p * p;
+        const double* Gr = G + (int64_t)rr * P2 * pp;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            int n = nb + i;
+            double val = 0.0;
+            if (rr < nrows && n < ncols) {
+                int c = n / nm, np = n - c * nm;
+                int a = modes[3 * np], b = modes[3 * np + 1], d = modes[3 * np + 2];
+                int cp = c * p;
+                val = Gr[(int64_t)pair_idx(a, b) * pp + cp + d] +
+                      Gr[(int64_t)pair_idx(a, d) * pp + cp + b] +
+                      Gr[(int64_t)pair_idx(b, d) * pp + cp + a];
+            }
+            r.v[i] = val;
+        }
+    }
+    __device__ void store(double* S, const Frag8& r) const { store_mrun(S, GB_LDB, r); }
+};
+
+__global__ void __launch_bounds__(GB_THREADS, 1)
+k_pair_contract(const MgRow* __restrict__ rows, int nrows, const double* __restrict__ q,
+                const double* __restrict__ G, const int* __restrict__ modes, int p, int P2,
+                int nm, int L, int l_min, double* __restrict__ Z) {
+    extern __shared__ __align__(16) double smem[];
+    const int m0 = blockIdx.y * GB_M, n0 = blockIdx.x * GB_N;
+    const int ncols = p * nm;
+    PA la;
+    {
+        int pr = m0 + (threadIdx.x & 127);
+        la.ok = pr < P2;
+        int a = 0, b = 0;
+        if (la.ok) pair_of(pr, a, b);
+        la.qa = q + (int64_t)a * L - l_min;
+        la.qb = q + (int64_t)b * L - l_min;
+        la.rows = rows;
+        la.nrows = nrows;
+    }
+    PB lb{G, modes, p, P2, nm, nrows, ncols, n0};
+    Acc acc;
+    gemm_mainloop((nrows + GB_K - 1) / GB_K, la, lb, smem, acc);
+    acc_foreach_pair(acc, [&](int m, int n, double v0, double v1) {
+        int pr = m0 + m, c = n0 + n;
+        if (pr < P2) {
+            double* z = Z + (int64_t)pr * ncols;
+            if (c < ncols) z[c] += v0;
+            if (c + 1 < ncols) z[c + 1] += v1;
+        }
+    });
+}
+
+// Γ[(ijk)][n'] = Z[ij][k][n'] + Z[ik][j][n'] + Z[jk][i][n']
+__global__ void k_final(const double* __restrict__ Z, const int* __restrict__ modes, int p,
+                        int nm, double* __restrict__ gamma) {
+    int64_t total = (int64_t)nm * nm;
+    const int64_t ncols = (int64_t)p * nm;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int n = (int)(i / nm), np = (int)(i % nm);
+        int a = modes[3 * n], b = modes[3 * n + 1], d = modes[3 * n + 2];
+        gamma[i] = Z[pair_idx(a, b) * ncols + (int64_t)d * nm + np] +
+                   Z[pair_idx(a, d) * ncols + (int64_t)b * nm + np] +
+                   Z[pair_idx(b, d) * ncols + (int64_t)a * nm + np];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+
+std::vector<double> log_factorials(int n) {
+    // t[k] = log(k!) accumulated left to right like np.cumsum(np.log(arange(1, size)))
+    std::vector<double> t(n + 1, 0.0);
+    for (int k = 1; k <= n; ++k) t[k] = t[k - 1] + std::log((double)k);
+    return t;
+}
+
+void plan_init(mg_plan* P, const double* q, const double* qt_host, const double* qt_dev,
+               const double* C, const double* v, const double* wr2, const int64_t* modes,
+               int p, int Nx, int n, int l_min, int l_max, int h2_mode) {
+    MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
+    MG_REQUIRE(p >= 1 && Nx >= 1 && n >= 1, "p, Nx, n must be >= 1");
+    MG_REQUIRE(h2_mode == MG_H2_GOSPER || h2_mode == MG_H2_EXACT, "unknown h2_mode");
+    MG_REQUIRE(p <= 64, "p_max > 64 not supported");
+    const int L = l_max - l_min + 1;
+    for (int i = 0; i < L; ++i) {
+        MG_REQUIRE(C[i] > 0, "power spectrum C_l must be strictly positive");
+        MG_REQUIRE(std::isfinite(C[i]) && std::isfinite(v[i]), "table contains non-finite values");
+    }
+    std::vector<int> md(3 * (size_t)n);
+    for (int i = 0; i < n; ++i) {
+        int64_t a = modes[3 * i], b = modes[3 * i + 1], c = modes[3 * i + 2];
+        MG_REQUIRE(0 <= a && a <= b && b <= c && c < p, "mapping triples must satisfy i<=j<=k<p");
+        md[3 * i] = (int)a; md[3 * i + 1] = (int)b; md[3 * i + 2] = (int)c;
+    }
+    P->p = p; P->Nx = Nx; P->nm = n; P->l_min = l_min; P->l_max = l_max; P->L = L;
+    P->h2_mode = h2_mode;
+    P->NxP = (int)round_up(Nx, GB_K);
+    P->P2 = p * (p + 1) / 2;
+    P->P8 = (int)round_up(p, 8);
+    P->rpt = std::max(1, GB_M / P->P8);
+    P->l0[l_min & 1] = l_min;
+    P->l0[(l_min + 1) & 1] = l_min + 1;
+    P->nclass[l_min & 1] = (L + 1) / 2;
+    P->nclass[(l_min + 1) & 1] = L / 2;
+    P->hC.assign(C, C + L);
+    P->hv.assign(v, v + L);
+
+    P->q.upload(q, (size_t)p * L);
+    P->C.upload(C, L);
+    P->v.upload(v, L);
+    P->wr2.upload(wr2, Nx);
+    P->modes.upload(md.data(), md.size());
+    std::vector<double> lf = log_factorials(3 * l_max + 2);
+    P->lf.upload(lf.data(), lf.size());
+
+    const size_t nq = (size_t)p * Nx * L;
+    DBuf<double> staged;
+    const double* qt_src = qt_dev;
+    if (!qt_src) {
+        staged.upload(qt_host, nq);
+        qt_src = staged.p;
+    }
+    P->QT.alloc((size_t)L * p * P->NxP);
+    P->WQT.alloc((size_t)L * p * P->NxP);
+    // classes: even-parity l first when l_min is even (class of l_min is class 0 in storage)
+    // storage index s(l) = (l - l_min)/2 for the parity of l_min, n0 + (l - l0')/2 otherwise
+    int n0 = (L + 1) / 2;
+    k_transpose_qt<<<1184, 256>>>(qt_src, P->wr2.p, p, Nx, P->NxP, L, l_min, l_min + 1, n0,
+                                  P->QT.p, P->WQT.p);
+    MG_LAUNCHED();
+    MG_CUDA(cudaDeviceSynchronize());
+}
+
+// Storage class offset (in l-slots) of parity `par` inside WQT.
+static inline int class_base(const mg_plan* P, int par) {
+    return par == (P->l_min & 1) ? 0 : (P->L + 1) / 2;
+}
+
+static inline bool lex_ge(int a2, int a3, int b2, int b3) {
+    return a2 > b2 || (a2 == b2 && a3 >= b3);
+}
+
+void build_rows(const mg_plan* P, int l2a, int l2b, const int* s, const int* e,
+                std::vector<MgRow>& rows) {
+    rows.clear();
+    const int lmin = P->l_min, lmax = P->l_max;
+    l2a = std::max(l2a, lmin);
+    l2b = std::min(l2b, lmax + 1);
+    for (int l2 = l2a; l2 < l2b; ++l2) {
+        if (l2 < s[0]) continue;  // no l1 <= l2 can reach the range start
+        for (int par = 0; par < 2; ++par) {
+            // l1 parity par  <=>  l3 = l2 + par (mod 2)
+            int l3top = std::min(2 * l2, lmax);
+            for (int l3 = l2 + par; l3 <= l3top; l3 += 2) {
+                int lo = std::max(lmin, l3 - l2);
+                int hi = l2;
+                int clo = lex_ge(l2, l3, s[1], s[2]) ? s[0] : s[0] + 1;
+                int chi = lex_ge(l2, l3, e[1], e[2]) ? e[0] - 1 : e[0];
+                lo = std::max(lo, clo);
+                hi = std::min(hi, chi);
+                if ((lo & 1) != par) ++lo;
+                if ((hi & 1) != par) --hi;
+                if (lo > hi) continue;
+                MgRow r;
+                r.l2 = l2; r.l3 = l3; r.par = par;
+                r.jlo = (lo - P->l0[par]) / 2;
+                r.jhi = (hi - P->l0[par]) / 2;
+                r.pad = 0;
+                rows.push_back(r);
+            }
+        }
+    }
+}
+
+// Batch geometry: K1/K2 work on nb1 rows at a time (H buffer), K3 on nb3 (G buffer).
+static void choose_batches(mg_plan* P) {
+    const double hrow = (double)P->p * P->p * P->NxP * 8.0;
+    const double grow = (double)P->P2 * P->p * P->p * 8.0;
+    int nb1 = (int)std::min(1024.0, std::max(16.0, 1.0e9 / hrow));
+    nb1 = std::max(16, nb1 / 16 * 16);
+    int nb3 = (int)std::min(2048.0, std::max((double)nb1, 1.5e9 / grow));
+    nb3 = std::max(nb1, nb3 / nb1 * nb1);
+    P->nb1 = nb1;
+    P->nb3 = nb3;
+}
+
+static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
+                         const std::vector<int64_t>& hzoff, cudaStream_t st,
+                         const int32_t* dt1, const int32_t* dt2, const int32_t* dt3,
+                         const int64_t* dpos, const double* ddup,
+                         const std::vector<int64_t>* tri_of_row) {
+    const int p = P->p, NxP = P->NxP, P2 = P->P2, nm = P->nm;
+    const int64_t nrows = (int64_t)hrows.size();
+    if (!P->nb1) choose_batches(P);
+    const int nb1 = P->nb1, nb3 = P->nb3;
+
+    // tiles: consecutive rows of one (l2, par) group, at most rpt per tile, per nb1-batch
+    std::vector<MgTile> tiles;
+    std::vector<int> tile_first;  // per nb1 batch
+    for (int64_t b1 = 0; b1 < nrows; b1 += nb1) {
+        int64_t e1 = std::min<int64_t>(b1 + nb1, nrows);
+        tile_first.push_back((int)tiles.size());
+        int64_t i = b1;
+        while (i < e1) {
+            MgTile t;
+            t.row0 = (int)i;
+            t.nrows = 0;
+            t.jlo = hrows[i].jlo;
+            t.jhi = hrows[i].jhi;
+            while (i < e1 && t.nrows < P->rpt && hrows[i].l2 == hrows[t.row0].l2 &&
+                   hrows[i].par == hrows[t.row0].par) {
+                t.jlo = std::min(t.jlo, hrows[i].jlo);
+                t.jhi = std::max(t.jhi, hrows[i].jhi);
+                ++t.nrows;
+                ++i;
+            }
+            tiles.push_back(t);
+        }
+    }
+    tile_first.push_back((int)tiles.size());
+
+    P->rows.upload(hrows.data(), hrows.size(), st);
+    P->zoff.upload(hzoff.data(), hzoff.size(), st);
+    P->tiles.upload(tiles.data(), tiles.size(), st);
+    int64_t maxzt = 0;
+    for (int64_t b1 = 0; b1 < nrows; b1 += nb1) {
+        int64_t e1 = std::min<int64_t>(b1 + nb1, nrows);
+        maxzt = std::max(maxzt, hzoff[e1] - hzoff[b1]);
+    }
+    P->ZT.ensure(std::max<int64_t>(maxzt, 1));
+    P->H.ensure((size_t)nb1 * p * p * NxP);
+    P->G.ensure((size_t)nb3 * P2 * p * p);
+    P->Z.ensure((size_t)P2 * p * nm);
+    MG_CUDA(cudaMemsetAsync(P->Z.p, 0, (size_t)P2 * p * nm * sizeof(double), st));
+    P->gamma.ensure((size_t)nm * nm);
+
+    static bool attr_done = false;
+    if (!attr_done) {
+        MG_CUDA(cudaFuncSetAttribute(k_run_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)GB_SMEM));
+        MG_CUDA(cudaFuncSetAttribute(k_x_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)GB_SMEM));
+        MG_CUDA(cudaFuncSetAttribute(k_pair_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)GB_SMEM));
+        attr_done = true;
+    }
+    DBuf<int> l0d;
+    l0d.upload(P->l0, 2, st);
+
+    double f_run = 0, f_x = 0, f_pair = 0;
+    int64_t launches = 0;
+    const int cb0 = class_base(P, 0), cb1 = class_base(P, 1);
+    const int l0e = P->l0[0], l0o = P->l0[1];
+    const int64_t ldb = (int64_t)p * NxP;
+    int bidx = 0;
+    for (int64_t b3 = 0; b3 < nrows; b3 += nb3) {
+        int64_t e3 = std::min<int64_t>(b3 + nb3, nrows);
+        for (int64_t b1 = b3; b1 < e3; b1 += nb1, ++bidx) {
+            int64_t e1 = std::min<int64_t>(b1 + nb1, e3);
+            int nb = (int)(e1 - b1);
+            const int64_t zbase = hzoff[b1];
+            if (!dt1) {
+                k_row_weights<<<nb, 128, 0, st>>>(P->rows.p + b1, P->zoff.p + b1, zbase, P->l_min,
+                                                  l0d.p, P->C.p, P->v.p, P->lf.p, P->h2_mode,
+                                                  P->ZT.p);
+            } else {
+                int64_t t0 = (*tri_of_row)[b1], t1 = (*tri_of_row)[e1];
+                MG_CUDA(cudaMemsetAsync(P->ZT.p, 0, (hzoff[e1] - zbase) * sizeof(double), st));
+                if (t1 > t0)
+                    k_scatter_weights<<<std::min<int64_t>((t1 - t0 + 255) / 256, 4096), 256, 0,
+                                        st>>>(dt1 + t0, dt2 + t0, dt3 + t0, dpos + t0, ddup + t0,
+                                              t1 - t0, zbase, P->l_min, P->C.p, P->v.p,
+                                              P->lf.p, P->h2_mode, P->ZT.p);
+            }
+            MG_LAUNCHED();
+            int tf = tile_first[bidx], tl = tile_first[bidx + 1];
+            dim3 g1(ceil_div(ldb, GB_N), tl - tf);
+            k_run_contract<<<g1, GB_THREADS, GB_SMEM, st>>>(
+                P->tiles.p + tf, P->rows.p, P->zoff.p, zbase, (int)b1, P->ZT.p, P->q.p,
+                P->WQT.p, p, P->P8, NxP, P->L, P->l_min, l0e, l0o, cb0, cb1, P->H.p);
+            MG_LAUNCHED();
+            dim3 g2(ceil_div(p * p, GB_N), ceil_div(P2, GB_M), nb);
+            k_x_contract<<<g2, GB_THREADS, GB_SMEM, st>>>(P->rows.p, (int)b1, (int)b3, P->QT.p,
+                                                          P->H.p, p, P2, NxP, P->l_min, P->G.p);
+            MG_LAUNCHED();
+            launches += 3;
+            for (int64_t r = b1; r < e1; ++r) {
+                double m = (double)(hrows[r].jhi - hrows[r].jlo + 1);
+                f_run += 2.0 * p * p * P->Nx * m;
+            }
+            f_x += 2.0 * P2 * p * p * P->Nx * nb;
+        }
+        dim3 g3(ceil_div((int64_t)p * nm, GB_N), ceil_div(P2, GB_M));
+        k_pair_contract<<<g3, GB_THREADS, GB_SMEM, st>>>(P->rows.p + b3, (int)(e3 - b3), P->q.p,
+                                                         P->G.p, P->modes.p, p, P2, nm, P->L,
+                                                         P->l_min, P->Z.p);
+        MG_LAUNCHED();
+        launches += 1;
+        f_pair += 2.0 * P2 * p * nm * (double)(e3 - b3);
+    }
+    k_final<<<std::min<int64_t>(((int64_t)nm * nm + 255) / 256, 4096), 256, 0, st>>>(
+        P->Z.p, P->modes.p, p, nm, P->gamma.p);
+    MG_LAUNCHED();
+    launches += 1;
+    P->flops_run = f_run;
+    P->flops_x = f_x;
+    P->flops_pair = f_pair;
+    P->launches = launches;
+    // keep l0d alive until the stream drains
+    MG_CUDA(cudaStreamSynchronize(st));
+}
+
+void execute_rows(mg_plan* P, const std::vector<MgRow>& rows, cudaStream_t st) {
+    std::vector<int64_t> zoff(rows.size() + 1, 0);
+    for (size_t i = 0; i < rows.size(); ++i)
+        zoff[i + 1] = zoff[i] + (rows[i].jhi - rows[i].jlo + 1);
+    if (rows.empty()) {
+        P->gamma.ensure((size_t)P->nm * P->nm);
+        MG_CUDA(cudaMemsetAsync(P->gamma.p, 0, (size_t)P->nm * P->nm * sizeof(double), st));
+        P->flops_run = P->flops_x = P->flops_pair = 0;
+        P->launches = 0;
+        return;
+    }
+    run_pipeline(P, rows, zoff, st, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
+                     int64_t count, cudaStream_t st) {
+    const int lmin = P->l_min, lmax = P->l_max;
+    struct T { int l2, l3, par, l1; };
+    std::vector<T> ts;
+    ts.reserve(count);
+    for (int64_t i = 0; i < count; ++i) {
+        int a = l1[i], b = l2[i], c = l3[i];
+        MG_REQUIRE(a <= b && b <= c, "permutation_multiplicity requires l1 <= l2 <= l3");
+        MG_REQUIRE(a >= lmin && c <= lmax, "triple outside [l_min, l_max]");
+        ts.push_back({b, c, a & 1, a});
+    }
+    std::sort(ts.begin(), ts.end(), [](const T& x, const T& y) {
+        if (x.l2 != y.l2) return x.l2 < y.l2;
+        if (x.par != y.par) return x.par < y.par;
+        if (x.l3 != y.l3) return x.l3 < y.l3;
+        return x.l1 < y.l1;
+    });
+    std::vector<MgRow> rows;
+    std::vector<int64_t> zoff(1, 0), tri_of_row(1, 0);
+    std::vector<int32_t> h1, h2, h3;
+    std::vector<int64_t> pos;
+    std::vector<double> dup;
+    size_t i = 0;
+    while (i < ts.size()) {
+        size_t j = i;
+        while (j < ts.size() && ts[j].l2 == ts[i].l2 && ts[j].l3 == ts[i].l3 &&
+               ts[j].par == ts[i].par)
+            ++j;
+        MgRow r;
+        r.l2 = ts[i].l2; r.l3 = ts[i].l3; r.par = ts[i].par; r.pad = 0;
+        r.jlo = (ts[i].l1 - P->l0[r.par]) / 2;
+        r.jhi = (ts[j - 1].l1 - P->l0[r.par]) / 2;
+        for (size_t k = i; k < j;) {
+            size_t k2 = k;
+            while (k2 < j && ts[k2].l1 == ts[k].l1) ++k2;  // duplicates add up
+            h1.push_back(ts[k].l1); h2.push_back(r.l2); h3.push_back(r.l3);
+            pos.push_back(zoff.back() + (ts[k].l1 - P->l0[r.par]) / 2 - r.jlo);
+            dup.push_back((double)(k2 - k));
+            k = k2;
+        }
+        rows.push_back(r);
+        zoff.push_back(zoff.back() + (r.jhi - r.jlo + 1));
+        tri_of_row.push_back((int64_t)h1.size());
+        i = j;
+    }
+    if (rows.empty()) {
+        execute_rows(P, rows, st);
+        return;
+    }
+    DBuf<int32_t> d1, d2, d3;
+    DBuf<int64_t> dp;
+    DBuf<double> dd;
+    d1.upload(h1.data(), h1.size(), st);
+    d2.upload(h2.data(), h2.size(), st);
+    d3.upload(h3.data(), h3.size(), st);
+    dp.upload(pos.data(), pos.size(), st);
+    dd.upload(dup.data(), dup.size(), st);
+    run_pipeline(P, rows, zoff, st, d1.p, d2.p, d3.p, dp.p, dd.p, &tri_of_row);
+}
+
+// ------------------------------------------------------------------------------------------
+// weights / enumeration on the device (mg_weights, mg_domain_triples)
+// ------------------------------------------------------------------------------------------
+__global__ void k_weights(const int64_t* __restrict__ l1_base, const int64_t* __restrict__ row_base,
+                          const int64_t* __restrict__ pair_off, int l_min, int l_max,
+                          int64_t begin, int64_t end, const double* __restrict__ C,
+                          const double* __restrict__ v, const double* __restrict__ lf, int mode,
+                          double* __restrict__ zm, int32_t* __restrict__ o1,
+                          int32_t* __restrict__ o2, int32_t* __restrict__ o3) {
+    const int L = l_max - l_min + 1;
+    for (int64_t idx = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < end;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = L;
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (l1_base[mid] <= idx) lo = mid; else hi = mid;
+        }
+        int64_t a = pair_off[lo], b = pair_off[lo + 1];
+        while (b - a > 1) {
+            int64_t mid = (a + b) >> 1;
+            if (row_base[mid] <= idx) a = mid; else b = mid;
+        }
+        int l1 = l_min + lo;
+        int l2 = l1 + (int)(a - pair_off[lo]);
+        int l3 = row_start(l1, l2) + 2 * (int)(idx - row_base[a]);
+        int64_t o = idx - begin;
+        if (o1) { o1[o] = l1; o2[o] = l2; o3[o] = l3; }
+        if (zm) zm[o] = zm_weight(mode, l1, l2, l3, C, v, l_min, lf);
+    }
+}
+
+void weights(int l_min, int l_max, const double* C, const double* v, int h2_mode,
+             int64_t begin, int64_t end, double* zm, int32_t* o1, int32_t* o2, int32_t* o3) {
+    DomainIndex D;
+    D.build(l_min, l_max);
+    if (end < 0 || end > D.count) end = D.count;
+    MG_REQUIRE(0 <= begin && begin <= end, "invalid flat range");
+    const int64_t n = end - begin;
+    if (n == 0) return;
+    const int L = l_max - l_min + 1;
+    DBuf<int64_t> b1, rb, po;
+    b1.upload(D.l1_base.data(), D.l1_base.size());
+    rb.upload(D.row_base.data(), D.row_base.size());
+    po.upload(D.pair_off.data(), D.pair_off.size());
+    DBuf<double> dC, dv, dlf, dz;
+    DBuf<int32_t> d1, d2, d3;
+    if (zm) {
+        if (h2_mode != MG_H2_GOSPER && h2_mode != MG_H2_EXACT) fail(MG_EINVAL, "unknown h2_mode");
+        for (int i = 0; i < L; ++i)
+            MG_REQUIRE(C[i] > 0, "power spectrum C_l must be strictly positive");
+        dC.upload(C, L);
+        dv.upload(v, L);
+        std::vector<double> lf = log_factorials(3 * l_max + 2);
+        dlf.upload(lf.data(), lf.size());
+        dz.alloc(n);
+    }
+    if (o1) { d1.alloc(n); d2.alloc(n); d3.alloc(n); }
+    int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    k_weights<<<grid, 256>>>(b1.p, rb.p, po.p, l_min, l_max, begin, end, dC.p, dv.p, dlf.p,
+                             h2_mode, dz.p, d1.p, d2.p, d3.p);
+    MG_LAUNCHED();
+    if (zm) MG_CUDA(cudaMemcpy(zm, dz.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (o1) {
+        MG_CUDA(cudaMemcpy(o1, d1.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        MG_CUDA(cudaMemcpy(o2, d2.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        MG_CUDA(cudaMemcpy(o3, d3.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Non-separable pointwise path (config 3)
+//   B(t,x) = Σ_n' α_n' Σ_6perms q̃q̃q̃  evaluated per (triple, x) — no factoring through Γ
+//   b[m]  += W_t zm_t P[m,t] Σ_x wr2_x B(t,x)
+// One CTA walks a strided subset of triples; per-CTA partial b's are summed in CTA order.
+// ------------------------------------------------------------------------------------------
+constexpr int NS_THREADS = 256;
+
+__global__ void __launch_bounds__(NS_THREADS)
+k_nonsep(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
+         const int32_t* __restrict__ t3, const double* __restrict__ W, int64_t count,
+         const double* __restrict__ QT, const double* __restrict__ wr2,
+         const double* __restrict__ q, const double* __restrict__ C, const double* __restrict__ v,
+         const double* __restrict__ lf, int mode, const double* __restrict__ alpha,
+         const int* __restrict__ modes, int p, int nm, int Nx, int NxP, int L, int l_min,
+         double* __restrict__ partial) {
+    extern __shared__ double sh[];
+    double* b_acc = sh;             // [nm]
+    double* red = sh + nm;          // [NS_THREADS/32]
+    int* md = reinterpret_cast<int*>(red + NS_THREADS / 32);  // [3*nm]
+    double* al = reinterpret_cast<double*>(md + 3 * nm + (3 * nm & 1));  // [nm]
+    for (int i = threadIdx.x; i < nm; i += blockDim.x) {
+        b_acc[i] = 0.0;
+        al[i] = alpha[i];
+        md[3 * i] = modes[3 * i];
+        md[3 * i + 1] = modes[3 * i + 1];
+        md[3 * i + 2] = modes[3 * i + 2];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t t = blockIdx.x; t < count; t += gridDim.x) {
+        const int a1 = t1[t], a2 = t2[t], a3 = t3[t];
+        const double* g1 = QT + (int64_t)(a1 - l_min) * p * NxP;
+        const double* g2 = QT + (int64_t)(a2 - l_min) * p * NxP;
+        const double* g3 = QT + (int64_t)(a3 - l_min) * p * NxP;
+        double xs = 0.0;
+        for (int x = threadIdx.x; x < Nx; x += blockDim.x) {
+            double Bx = 0.0;
+            for (int m = 0; m < nm; ++m) {
+                int i = md[3 * m], j = md[3 * m + 1], k = md[3 * m + 2];
+                double i1 = g1[i * NxP + x], j1 = g1[j * NxP + x], k1 = g1[k * NxP + x];
+                double i2 = g2[i * NxP + x], j2 = g2[j * NxP + x], k2 = g2[k * NxP + x];
+                double i3 = g3[i * NxP + x], j3 = g3[j * NxP + x], k3 = g3[k * NxP + x];
+                double f = i1 * (j2 * k3 + k2 * j3) + j1 * (i2 * k3 + k2 * i3) +
+                           k1 * (i2 * j3 + j2 * i3);
+                Bx += al[m] * f;
+            }
+            xs += wr2[x] * Bx;
+        }
+        for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+        if (lane == 0) red[warp] = xs;
+        __syncthreads();
+        double X = 0.0;
+        for (int w = 0; w < NS_THREADS / 32; ++w) X += red[w];
+        double wz = W[t] * zm_weight(mode, a1, a2, a3, C, v, l_min, lf) * X;
+        for (int m = threadIdx.x; m < nm; m += blockDim.x) {
+            int i = md[3 * m], j = md[3 * m + 1], k = md[3 * m + 2];
+            const double* qi = q + (int64_t)i * L - l_min;
+            const double* qj = q + (int64_t)j * L - l_min;
+            const double* qk = q + (int64_t)k * L - l_min;
+            double P = qi[a1] * (qj[a2] * qk[a3] + qk[a2] * qj[a3]) +
+                       qj[a1] * (qi[a2] * qk[a3] + qk[a2] * qi[a3]) +
+                       qk[a1] * (qi[a2] * qj[a3] + qj[a2] * qi[a3]);
+            b_acc[m] += wz * P;
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < nm; i += blockDim.x) partial[(int64_t)blockIdx.x * nm + i] = b_acc[i];
+}
+
+__global__ void k_sum_partials(const double* __restrict__ partial, int nblocks, int nm,
+                               double* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nm) return;
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += partial[(int64_t)b * nm + i];
+    out[i] = s;
+}
+
+void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l2,
+            const int32_t* l3, const double* W, int64_t count, double* b, cudaStream_t st) {
+    const int nm = P->nm;
+    for (int64_t i = 0; i < count; ++i) {
+        MG_REQUIRE(l1[i] <= l2[i] && l2[i] <= l3[i], "triples must satisfy l1 <= l2 <= l3");
+        MG_REQUIRE(l1[i] >= P->l_min && l3[i] <= P->l_max, "triple outside [l_min, l_max]");
+    }
+    DBuf<int32_t> d1, d2, d3;
+    DBuf<double> dW, dal, dout;
+    d1.upload(l1, count, st);
+    d2.upload(l2, count, st);
+    d3.upload(l3, count, st);
+    dW.upload(W, count, st);
+    dal.upload(alpha, nm, st);
+    const int nblocks = 148 * 8;
+    DBuf<double> part((size_t)nblocks * nm);
+    dout.alloc(nm);
+    size_t shm = (size_t)nm * 8 + NS_THREADS / 32 * 8 + (3 * nm + 1) * 4 + 8 + (size_t)nm * 8;
+    if (shm > 48 * 1024)
+        MG_CUDA(cudaFuncSetAttribute(k_nonsep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    k_nonsep<<<nblocks, NS_THREADS, shm, st>>>(d1.p, d2.p, d3.p, dW.p, count, P->QT.p, P->wr2.p,
+                                                P->q.p, P->C.p, P->v.p, P->lf.p, P->h2_mode,
+                                                dal.p, P->modes.p, P->p, nm, P->Nx, P->NxP,
+                                                P->L, P->l_min, part.p);
+    MG_LAUNCHED();
+    k_sum_partials<<<(nm + 127) / 128, 128, 0, st>>>(part.p, nblocks, nm, dout.p);
+    MG_LAUNCHED();
+    MG_CUDA(cudaMemcpyAsync(b, dout.p, nm * sizeof(double), cudaMemcpyDeviceToHost, st));
+    MG_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace mg

@@ -1,0 +1,60 @@
+// mg_gamma.cuh — the resident Γ plan (shared by mg_gamma.cu and mg_api.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "mg_common.cuh"
+#include "mg_domain.cuh"
+
+// One (l2,l3)-row of the factorised sum: l1 runs over l0[par] + 2 j, j in [jlo, jhi].
+// (par = l1 parity; for the reference domain par = (l2 + l3) & 1.)
+struct MgRow {
+    int l2, l3, par, jlo, jhi, pad;
+};
+// One M-tile of the run-contraction GEMM: up to `rpt` consecutive rows of one parity class.
+struct MgTile {
+    int row0, nrows, jlo, jhi;
+};
+
+struct mg_plan {
+    int device = 0;
+    int p = 0, Nx = 0, NxP = 0, nm = 0, l_min = 2, l_max = 2, L = 0, h2_mode = 0;
+    int P2 = 0;        // p(p+1)/2 unordered basis pairs
+    int P8 = 0;        // p rounded up to 8 (slot stride of the run-contraction tile)
+    int rpt = 0;       // rows per run-contraction tile = 128 / P8
+    int l0[2] = {0, 0};      // first l of each parity class
+    int nclass[2] = {0, 0};  // number of l in each parity class
+    mg::DBuf<double> q, QT, WQT, C, v, lf, wr2;
+    mg::DBuf<int> modes;  // [nm][3]
+    // scratch
+    mg::DBuf<double> ZT, H, G, Z, gamma;
+    mg::DBuf<MgRow> rows;
+    mg::DBuf<int64_t> zoff;
+    mg::DBuf<MgTile> tiles;
+    int nb1 = 0, nb3 = 0;  // rows per run/x-contraction batch, rows per pair-contraction batch
+    // stats of the last execute
+    double flops_run = 0, flops_x = 0, flops_pair = 0;
+    int64_t launches = 0;
+    // host copies (for the direct/nonsep paths)
+    std::vector<double> hC, hv;
+};
+
+namespace mg {
+void plan_init(mg_plan* P, const double* q, const double* qt_host, const double* qt_dev,
+               const double* C, const double* v, const double* wr2, const int64_t* modes,
+               int p, int Nx, int n, int l_min, int l_max, int h2_mode);
+// Rows of the l2-slab [l2a, l2b) clipped to the flat range (s1,s2,s3) <= t < (e1,e2,e3).
+void build_rows(const mg_plan* P, int l2a, int l2b, const int* s, const int* e,
+                std::vector<MgRow>& rows);
+void execute_rows(mg_plan* P, const std::vector<MgRow>& rows, cudaStream_t st);
+void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
+                     int64_t count, cudaStream_t st);
+void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l2,
+            const int32_t* l3, const double* W, int64_t count, double* b, cudaStream_t st);
+void weights(int l_min, int l_max, const double* C, const double* v, int h2_mode,
+             int64_t begin, int64_t end, double* zm, int32_t* o1, int32_t* o2, int32_t* o3);
+std::vector<double> log_factorials(int n);
+}  // namespace mg

@@ -1,0 +1,221 @@
+"""GPU parity of the separable Γ path against the oracle and the reference's golden vectors.
+
+Mirrors the reference's hot-path tests (pkg/tests/test_engine3d.py, test_geometry.py,
+test_acceptance.py criteria 3, 4, 7) but runs the CUDA library through the drop-in API.
+Tolerances: weights and enumeration bit-exact; Γ relative Frobenius <= 1e-10 (north_star);
+the reference's own 1e-12 relative_gap is also asserted where it applies.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import frob_rel, gap_rel
+from oracle import ref
+from paper_1503_08809_b200 import (BasisTables, DomainRange, GammaPlan, ModeMapping,
+                                   RadialGrid, domain_count, domain_triples, gamma3d_matrix,
+                                   triple_weights, x_weights)
+from paper_1503_08809_b200.configs import host_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def desk_problem(g, tag):
+    lmin, lmax = (int(x) for x in g[f"{tag}_lrange"])
+    t = BasisTables(g[f"{tag}_q"], g[f"{tag}_qt"], g[f"{tag}_C"], g[f"{tag}_v"], lmin, lmax)
+    m = ModeMapping(g[f"{tag}_entries"], t.p_max)
+    r = RadialGrid(g[f"{tag}_r"])
+    return t, m, r
+
+
+class TestDomainAndWeights:
+    def test_counts(self, g_domain):
+        for m, c in zip(g_domain["count_lmax"], g_domain["count"]):
+            assert domain_count(2, int(m)) == int(c)
+
+    def test_enumeration_golden(self, g_domain):
+        got = np.stack(domain_triples(2, 4), 1)
+        assert np.array_equal(got, g_domain["triples_2_4"])
+        a, b, c = domain_triples(3, 40)
+        assert np.array_equal(a, g_domain["l1_3_40"])
+        assert np.array_equal(b, g_domain["l2_3_40"])
+        assert np.array_equal(c, g_domain["l3_3_40"])
+
+    @pytest.mark.parametrize("lmax,begin,end", [(200, 0, None), (2000, 0, 200000),
+                                                 (2000, 167_000_000, 167_250_000),
+                                                 (3000, 1_128_000_000, None)])
+    def test_enumeration_vs_oracle(self, lmax, begin, end):
+        end = domain_count(2, lmax) if end is None else end
+        got = domain_triples(2, lmax, begin, end)
+        want = ref.domain_triples(2, lmax, begin, end)
+        for x, y in zip(got, want):
+            assert np.array_equal(x, y)
+
+    def test_weights_bit_exact_golden(self, g_domain):
+        zm = triple_weights(g_domain["zm64_C"], g_domain["zm64_v"], 2, 64)
+        assert np.array_equal(zm, g_domain["zm64"])          # bitwise, NumPy order
+
+    def test_weights_exact_mode(self, g_domain):
+        zm = triple_weights(g_domain["zm64_C"], g_domain["zm64_v"], 2, 64, h2_mode="exact")
+        assert np.max(np.abs(zm / g_domain["zm64_exact"] - 1)) < 1e-13
+
+    @pytest.mark.parametrize("lmax,begin,end", [(200, 0, None), (2000, 250_000_000, 250_400_000)])
+    def test_weights_bit_exact_large(self, lmax, begin, end):
+        rng = np.random.default_rng(11)
+        C = rng.uniform(1e-6, 1e-1, lmax - 1)
+        v = (2.0 * np.arange(2, lmax + 1) + 1.0) ** (1.0 / 6.0)
+        end = domain_count(2, lmax) if end is None else end
+        zm = triple_weights(C, v, 2, lmax, begin, end)
+        l1, l2, l3 = ref.domain_triples(2, lmax, begin, end)
+        assert np.array_equal(zm, ref.zm_c(2, l1, l2, l3, C, v))
+        assert np.array_equal(zm, ref.triple_zm(2, l1, l2, l3, C, v))
+
+    def test_zm_222_unit(self, g_domain):
+        zm = triple_weights(np.ones(1), np.ones(1), 2, 2)
+        assert zm[0] == g_domain["z222_unit"]                 # mult(2,2,2) = 1
+        assert abs(zm[0] - 0.016088) < 2e-6                   # test_geometry.py:175-179
+
+    def test_rejects_nonpositive_spectrum(self):
+        with pytest.raises(ValueError):
+            triple_weights(np.zeros(1), np.ones(1), 2, 2)
+
+
+class TestGammaDesk:
+    """test_engine3d.py TestBlockedVsNaive / TestOrderedEnumeration on the GPU."""
+
+    @pytest.mark.parametrize("tag", ["desk", "desk32", "small12"])
+    def test_matches_reference(self, g_desk, tag):
+        t, m, r = desk_problem(g_desk, tag)
+        got = gamma3d_matrix(t, m, r).values
+        assert gap_rel(got, g_desk[f"{tag}_gamma"]) < 1e-12
+        assert frob_rel(got, g_desk[f"{tag}_gamma"]) < 1e-12
+
+    def test_matches_naive(self, g_desk):
+        t, m, r = desk_problem(g_desk, "desk")
+        assert gap_rel(gamma3d_matrix(t, m, r).values, g_desk["desk_naive"]) < 1e-12
+
+    def test_ordered_equals_unordered(self, g_desk):
+        t, m, r = desk_problem(g_desk, "small12")
+        assert gap_rel(gamma3d_matrix(t, m, r).values, g_desk["small12_unordered"]) < 1e-12
+
+    @pytest.mark.parametrize("integrator", ["hermite", "spline"])
+    def test_other_integrators(self, g_desk, integrator):
+        t, m, r = desk_problem(g_desk, "desk")
+        got = gamma3d_matrix(t, m, r, integrator=integrator).values
+        assert gap_rel(got, g_desk[f"desk_{integrator}"]) < 1e-12
+
+    def test_exact_mode(self, g_desk):
+        t, m, r = desk_problem(g_desk, "desk")
+        got = gamma3d_matrix(t, m, r, h2_mode="exact").values
+        assert gap_rel(got, g_desk["desk_exact"]) < 1e-12
+
+    def test_block_and_workers_are_metadata(self, g_desk):
+        t, m, r = desk_problem(g_desk, "desk32")
+        a = gamma3d_matrix(t, m, r, block=7, workers=4)
+        assert gap_rel(a.values, g_desk["desk32_w4"]) < 1e-12
+        assert a.meta["block"] == 7 and a.meta["workers"] == 4
+        assert a.meta["engine"] == "modal3d" and a.meta["tables"] == t.fingerprint()
+
+    def test_bitwise_reproducible(self, g_desk):
+        t, m, r = desk_problem(g_desk, "desk32")
+        a = gamma3d_matrix(t, m, r).values
+        b = gamma3d_matrix(t, m, r).values
+        assert np.array_equal(a, b)
+
+    def test_errors(self, g_desk):
+        t, m, r = desk_problem(g_desk, "desk")
+        with pytest.raises(ValueError):
+            gamma3d_matrix(t, m, r, h2_mode="asymptotic")
+        with pytest.raises(ValueError):
+            gamma3d_matrix(t, m, r, block=0)
+
+    def test_explicit_noncontiguous_domain(self, g_desk):
+        t, m, r = desk_problem(g_desk, "desk32")
+        l1, l2, l3 = ref.domain_triples(2, 32)
+        keep = (np.arange(l1.size) % 3) != 1
+
+        class Dom:
+            pass
+
+        d = Dom()
+        d.l1, d.l2, d.l3 = l1[keep], l2[keep], l3[keep]
+        d.count = int(keep.sum())
+        got = gamma3d_matrix(t, m, r, domain=d).values
+        want = ref.sweep_triples(t.q, t.q_tilde, t.C, t.v, x_weights(r.r), m.entries, 2,
+                                 d.l1, d.l2, d.l3)
+        assert frob_rel(got, want) < 1e-12
+
+    def test_empty_range(self, g_desk):
+        t, m, r = desk_problem(g_desk, "desk")
+        got = gamma3d_matrix(t, m, r, domain=DomainRange(2, 16, 5, 5)).values
+        assert not got.any()
+
+
+class TestGammaC0:
+    def tables(self, g_c0):
+        hi = host_inputs("c0")
+        t = BasisTables(hi.q, g_c0["qt"], g_c0["C"], hi.v, 2, 200)
+        return t, ModeMapping(hi.entries, hi.spec.p), RadialGrid(hi.x)
+
+    def test_full_gamma(self, g_c0):
+        t, m, r = self.tables(g_c0)
+        got = gamma3d_matrix(t, m, r).values
+        assert frob_rel(got, g_c0["gamma"]) < 1e-10
+        assert gap_rel(got, g_c0["gamma"]) < 1e-12
+
+    @pytest.mark.parametrize("a,b", [(0, 1000), (1000, 20000), (200000, 348151)])
+    def test_flat_range_partials(self, g_c0, a, b):
+        t, m, r = self.tables(g_c0)
+        got = gamma3d_matrix(t, m, r, domain=DomainRange(2, 200, a, b)).values
+        assert frob_rel(got, g_c0[f"partial_{a}_{b}"]) < 1e-10
+
+    def test_exact_mode(self, g_c0):
+        t, m, r = self.tables(g_c0)
+        got = gamma3d_matrix(t, m, r, h2_mode="exact").values
+        assert frob_rel(got, g_c0["gamma_exact"]) < 1e-10
+
+    def test_slabs_add_up(self, g_c0):
+        t, m, r = self.tables(g_c0)
+        plan = GammaPlan.from_tables(t, m, r)
+        total = np.zeros((56, 56))
+        for a, b in ((2, 60), (60, 131), (131, 201)):
+            plan.execute(a, b)
+            total += plan.fetch()
+        assert frob_rel(total, g_c0["gamma"]) < 1e-12
+
+
+class TestGammaLarge:
+    """Config-1 scale: flat-range partials vs the oracle on the same (GPU-built) q̃."""
+
+    @pytest.fixture(scope="class")
+    def c1(self):
+        from paper_1503_08809_b200 import build_qtilde
+        hi = host_inputs("c1")
+        C, qt = build_qtilde(hi)
+        return hi, C, qt
+
+    @pytest.mark.parametrize("frac", [0.1, 0.5, 0.9])
+    def test_partial_vs_oracle(self, c1, frac):
+        hi, C, qt = c1
+        total = domain_count(2, hi.l_max)
+        a = int(frac * total)
+        b = a + 3000
+        t = BasisTables(hi.q, qt, C, hi.v, 2, hi.l_max)
+        m = ModeMapping(hi.entries, hi.spec.p)
+        got = gamma3d_matrix(t, m, RadialGrid(hi.x), domain=DomainRange(2, hi.l_max, a, b)).values
+        want = ref.gamma3d(hi.q, qt, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max, a, b)
+        assert frob_rel(got, want) < 1e-10
+
+    def test_slab_partition_is_exact(self, c1):
+        """Size-independent property at full c1 size: l2 slabs sum to the full Γ."""
+        hi, C, qt = c1
+        plan = GammaPlan(hi.q, qt, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max)
+        plan.execute()
+        full = plan.fetch()
+        bounds = [2, 700, 1300, hi.l_max + 1]
+        parts = []
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            plan.execute(a, b)
+            parts.append(plan.fetch())
+        assert frob_rel(sum(parts), full) < 1e-12
+        plan.execute()
+        assert np.array_equal(plan.fetch(), full)              # bitwise reproducible
