@@ -1,0 +1,358 @@
+"""Γ projection benchmark (BASELINE.json metric: (l-triple·x·mode) FP64 updates/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl b200|reference]
+
+One "step" = one full separable Γ (BASELINE config 1 by default: l_max=2000, p=15 -> 680
+modes, Nx=500, 334,831,501 ordered triples) with q̃ already resident in HBM.  For N>1
+(launched by torchrun) every rank computes one cost-balanced l2 slab and the partial Γ's
+are all-gathered over NCCL and summed in rank order; the step time is the max over ranks.
+
+`--impl reference` times the reference algorithm on the host CPU cores instead (the
+reference is pure Python/NumPy and cannot be compiled; its NumPy restatement in oracle/ is
+the same code path, pinned bit-for-bit to the reference on config 0): rank 0 only, each
+step a bounded flat-range sample of the same config.
+"""
+
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OMP_NUM_THREADS", "1")        # before numpy: CPU baseline is 1 thread/worker
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import argparse
+import json
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA peak on this pool's B200 (profiles/r01_fp64_peak.txt)
+FP64_PEAK_SRC = "measured: tools/fp64_peak.cu DMMA.8x8x4 microbenchmark, profiles/r01_fp64_peak.txt"
+UPDATE_FLOPS = 6.0       # algorithmic FP64 FLOPs per (l-triple, x, mode) update
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-reps", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu),
+                                      f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def total_updates(spec):
+    from paper_1503_08809_b200 import domain_count
+    T = domain_count(2, spec.l_max)
+    n = (spec.p * (spec.p + 1) * (spec.p + 2)) // 6
+    return T, T * spec.n_x * n, n
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_rate(hi, qt_host, C, seconds, cores):
+    """Oracle port (= reference _sweep_chunk code path) on a bounded flat slice, all cores."""
+    from oracle import ref
+    from paper_1503_08809_b200 import domain_count
+
+    T = domain_count(2, hi.l_max)
+    n = hi.entries.shape[0]
+    per_core = 1.5e7                                  # upd/s/core, SURVEY §6 (c0..c4 slices)
+    S = max(cores * 8, int(seconds * per_core * cores / (hi.x.size * n)))
+    S = min(S, T)
+    a = T // 2
+    t0 = time.perf_counter()
+    ref.gamma3d(hi.q, qt_host, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max, a, a + S,
+                workers=cores, block=64)
+    dt = time.perf_counter() - t0
+    return S * hi.x.size * n / dt, S, a, dt
+
+
+def run_b200(args):
+    import torch
+
+    from paper_1503_08809_b200 import (BasisTables, GammaPlan, ModeMapping, RadialGrid,
+                                       build_qtilde_device, gamma3d_matrix, slab_plan)
+    from paper_1503_08809_b200.configs import CONFIGS, host_inputs
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = CONFIGS[args.config]
+    hi = host_inputs(spec)
+    T, U, nmodes = total_updates(spec)
+    stream = torch.cuda.current_stream()
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    C_dev, qt_dev = build_qtilde_device(hi, device=local, stream=stream)
+    torch.cuda.synchronize()
+    t_qtilde = time.perf_counter() - t0
+    C = C_dev.cpu().numpy()
+    plan = GammaPlan(hi.q, qt_dev, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max, device=local)
+    bounds = slab_plan(2, hi.l_max, spec.p, spec.n_x, world)
+    a, b = bounds[rank], bounds[rank + 1]
+    out = torch.empty((nmodes, nmodes), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2
+
+    def step():
+        plan.execute(a, b, out=out, stream=stream)
+        if world > 1:
+            from paper_1503_08809_b200.dist import merge_rank_partials
+            return merge_rank_partials(out)
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    plan.set_profile(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                            # L2 flush between timed steps (untimed)
+            evs[i][0].record(stream)
+            res = step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms_steps = [s.elapsed_time(e) for s, e in evs]
+    ms = float(np.mean(ms_steps))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    kms = plan.kernel_ms()
+    stats = plan.stats()
+    gamma_dev = res.clone()
+
+    # ---- end-to-end through the public drop-in API with host buffers ----
+    qt_host = qt_dev.cpu().numpy()
+    tables = BasisTables(hi.q, qt_host, C, hi.v, 2, hi.l_max)
+    mapping = ModeMapping(hi.entries, spec.p)
+    grid = RadialGrid(hi.x)
+    h2d = sum(x.nbytes for x in (hi.q, qt_host, C, hi.v, hi.wr2, hi.entries))
+    d2h = nmodes * nmodes * 8
+    e2e_t = []
+    for _ in range(max(1, args.e2e_reps)):
+        if world > 1:
+            from paper_1503_08809_b200.dist import gamma3d_matrix_distributed
+            torch.distributed.barrier()
+            t1 = time.perf_counter()
+            g = gamma3d_matrix_distributed(tables, mapping, grid, device=local)
+        else:
+            t1 = time.perf_counter()
+            g = gamma3d_matrix(tables, mapping, grid, device=local)
+        e2e_t.append(time.perf_counter() - t1)
+    e2e_s = float(np.mean(e2e_t))
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_match = bool(np.allclose(g.values, gamma_dev.cpu().numpy(), rtol=1e-12, atol=0))
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+
+    fams = {"run": stats["flops_run"], "x": stats["flops_x"], "pair": stats["flops_pair"]}
+    names = {"run": "k_run_contract", "x": "k_x_contract", "pair": "k_pair_contract"}
+    dom = max(fams, key=lambda f: kms[f])
+    steps = args.steps
+    k_time = kms[dom] / 1e3 / steps
+    achieved = fams[dom] / k_time / 1e12 if k_time > 0 else 0.0
+    exec_flops = sum(fams.values())
+    step_s = ms / 1e3
+    line = {
+        "metric": "Γ projection: (l-triple·x·mode) FP64 updates/s",
+        "value": U / step_s,
+        "unit": "updates/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json config shapes; q̃ built on-device from "
+                "Bessel/transfer inputs)",
+        "config": {"workload": f"separable Γ, BASELINE config {args.config[1:]}: "
+                               f"l_max={spec.l_max}, p={spec.p} -> {nmodes} modes, "
+                               f"Nx={spec.n_x}, Nk={spec.n_k}, T={T} ordered triples",
+                   "updates_per_step": U, "parallelism": f"l2-slab x{world}",
+                   "l2_flush": "256 MiB write between timed steps (untimed); q̃ tables "
+                               "(QT+WQT 2x128 MB) exceed L2"},
+        "s_per_gamma": step_s,
+        "effective_fp64_tflops": UPDATE_FLOPS * U / step_s / 1e12,
+        "effective_fp64_frac": UPDATE_FLOPS * U / step_s / 1e12 / FP64_PEAK_TFLOPS,
+        "executed_fp64_tflops": exec_flops / world / step_s / 1e12 if world == 1 else None,
+        "executed_fp64_frac": exec_flops / step_s / 1e12 / FP64_PEAK_TFLOPS if world == 1
+        else None,
+        "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "peak_source": FP64_PEAK_SRC + " (MEASURED_PEAKS.json has no FP64 entry)",
+                     "kernel_ms_per_step": {k: v / steps for k, v in kms.items()},
+                     "kernel_share": {k: v / max(sum(kms.values()), 1e-9)
+                                      for k, v in kms.items()}},
+        "e2e": {"value": U / e2e_s, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "s_per_gamma": e2e_s,
+                "matches_device_result": e2e_match},
+        "gpu_launches": int(stats["launches"]) + (0 if world == 1 else 0),
+        "qtilde_build_s": t_qtilde,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        rate, S, a0, dt = cpu_rate(hi, qt_host, C, args.cpu_seconds, cores)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": "updates/s", "cores": cores, "kind": "port",
+            "sample": f"oracle port of engine3d._sweep_chunk (B=64, fork pool of {cores}) over "
+                      f"flat range [{a0}, {a0 + S}) of config {args.config[1:]} "
+                      f"({S} triples, {dt:.1f} s); extrapolated s/Γ = {U / rate:.3g}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from multiprocessing import get_context
+
+    from oracle import qtilde_ref, ref
+    from paper_1503_08809_b200.configs import CONFIGS, host_inputs
+
+    spec = CONFIGS[args.config]
+    hi = host_inputs(spec)
+    T, U, nmodes = total_updates(spec)
+    cores = os.cpu_count() or 1
+    per_core = 1.5e7
+    S = max(cores * 8, int(args.cpu_seconds * per_core * cores / (spec.n_x * nmodes)))
+    S = min(S, T)
+    a = T // 2
+    l1, l2, l3 = ref.domain_triples(2, spec.l_max, a, a + S)
+    ells = np.unique(np.concatenate([l1, l2, l3]))
+    d = qtilde_ref.delta_table(hi.k, hi.eps, 2, spec.l_max)
+    C = qtilde_ref.c_ell(d, hi.k, hi.wk)
+    chunks = np.array_split(ells, cores)
+    with get_context("fork").Pool(cores) as pool:
+        parts = pool.starmap(qtilde_ref.qtilde,
+                             [(hi.k, hi.wk, hi.x, hi.qk, d, 2, spec.l_max, list(c))
+                              for c in chunks])
+    qt = sum(parts)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ref.gamma3d(hi.q, qt, C, hi.v, hi.wr2, hi.entries, 2, spec.l_max, a, a + S,
+                    workers=cores, block=64)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    rate = S * spec.n_x * nmodes / dt
+    sample = (f"reference algorithm (NumPy restatement of engine3d._sweep_chunk, bit-identical "
+              f"to cmbproj on config 0) over flat range [{a}, {a + S}) of config "
+              f"{args.config[1:]} ({S} triples), fork pool of {cores}, B=64")
+    line = {
+        "metric": "Γ projection: (l-triple·x·mode) FP64 updates/s", "value": rate,
+        "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config shapes)",
+        "config": {"workload": f"separable Γ, BASELINE config {args.config[1:]} (bounded "
+                               f"flat-range sample per step)", "updates_per_step": S * spec.n_x * nmodes,
+                   "parallelism": f"cpu x{cores}"},
+        "impl": "reference",
+        "s_per_gamma_extrapolated": U / rate,
+        "cpu_baseline": {"value": rate, "unit": "updates/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -44,6 +44,8 @@ _SIGS = {
     "mg_plan_execute": (_i, [_vp, _i, _i, _vp, _vp]),
     "mg_plan_fetch": (_i, [_vp, _vp, _vp]),
     "mg_plan_stats": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "mg_plan_set_profile": (_i, [_vp, _i]),
+    "mg_plan_kernel_ms": (_i, [_vp, _vp]),
     "mg_plan_destroy": (None, [_vp]),
     "mg_build_qtilde": (_i, [_vp, _vp, _i, _vp, _i, _vp, _vp, _i, _i, _i, _d, _d, _d, _i, _vp,
                              _vp, _vp]),

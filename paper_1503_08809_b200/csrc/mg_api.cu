@@ -190,6 +190,21 @@ int mg_plan_stats(mg_plan* P, double* f_run, double* f_x, double* f_pair, int64_
     });
 }
 
+int mg_plan_set_profile(mg_plan* P, int on) {
+    return guarded([&] {
+        MG_REQUIRE(P, "null plan");
+        P->profile = on != 0;
+        for (double& m : P->prof_ms) m = 0.0;
+    });
+}
+
+int mg_plan_kernel_ms(mg_plan* P, double* ms) {
+    return guarded([&] {
+        MG_REQUIRE(P && ms, "null argument");
+        for (int i = 0; i < 5; ++i) ms[i] = P->prof_ms[i];
+    });
+}
+
 void mg_plan_destroy(mg_plan* P) {
     if (!P) return;
     int prev = -1;

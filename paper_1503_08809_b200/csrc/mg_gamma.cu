@@ -479,6 +479,32 @@ static void choose_batches(mg_plan* P) {
     P->nb3 = nb3;
 }
 
+// Optional per-family kernel timing (mg_plan_set_profile): one event before every launch,
+// duration of launch i = event[i+1] - event[i] on the launching stream.
+static void prof_mark(mg_plan* P, int tag, cudaStream_t st) {
+    if (!P->profile) return;
+    if (P->prof_used == P->prof_events.size()) {
+        cudaEvent_t e;
+        MG_CUDA(cudaEventCreate(&e));
+        P->prof_events.push_back(e);
+    }
+    MG_CUDA(cudaEventRecord(P->prof_events[P->prof_used], st));
+    P->prof_tags.push_back(tag);
+    ++P->prof_used;
+}
+
+static void prof_collect(mg_plan* P) {
+    if (!P->profile) return;
+    for (size_t i = 0; i + 1 < P->prof_used; ++i) {
+        float ms = 0.f;
+        MG_CUDA(cudaEventElapsedTime(&ms, P->prof_events[i], P->prof_events[i + 1]));
+        int tag = P->prof_tags[i];
+        if (tag >= 0 && tag < 5) P->prof_ms[tag] += ms;
+    }
+    P->prof_used = 0;
+    P->prof_tags.clear();
+}
+
 static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                          const std::vector<int64_t>& hzoff, cudaStream_t st,
                          const int32_t* dt1, const int32_t* dt2, const int32_t* dt3,
@@ -554,6 +580,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             int64_t e1 = std::min<int64_t>(b1 + nb1, e3);
             int nb = (int)(e1 - b1);
             const int64_t zbase = hzoff[b1];
+            prof_mark(P, 0, st);
             if (!dt1) {
                 k_row_weights<<<nb, 128, 0, st>>>(P->rows.p + b1, P->zoff.p + b1, zbase, P->l_min,
                                                   l0d.p, P->C.p, P->v.p, P->lf.p, P->h2_mode,
@@ -570,11 +597,13 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             MG_LAUNCHED();
             int tf = tile_first[bidx], tl = tile_first[bidx + 1];
             dim3 g1(ceil_div(ldb, GB_N), tl - tf);
+            prof_mark(P, 1, st);
             k_run_contract<<<g1, GB_THREADS, GB_SMEM, st>>>(
                 P->tiles.p + tf, P->rows.p, P->zoff.p, zbase, (int)b1, P->ZT.p, P->q.p,
                 P->WQT.p, p, P->P8, NxP, P->L, P->l_min, l0e, l0o, cb0, cb1, P->H.p);
             MG_LAUNCHED();
             dim3 g2(ceil_div(p * p, GB_N), ceil_div(P2, GB_M), nb);
+            prof_mark(P, 2, st);
             k_x_contract<<<g2, GB_THREADS, GB_SMEM, st>>>(P->rows.p, (int)b1, (int)b3, P->QT.p,
                                                           P->H.p, p, P2, NxP, P->l_min, P->G.p);
             MG_LAUNCHED();
@@ -586,6 +615,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             f_x += 2.0 * P2 * p * p * P->Nx * nb;
         }
         dim3 g3(ceil_div((int64_t)p * nm, GB_N), ceil_div(P2, GB_M));
+        prof_mark(P, 3, st);
         k_pair_contract<<<g3, GB_THREADS, GB_SMEM, st>>>(P->rows.p + b3, (int)(e3 - b3), P->q.p,
                                                          P->G.p, P->modes.p, p, P2, nm, P->L,
                                                          P->l_min, P->Z.p);
@@ -593,9 +623,11 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         launches += 1;
         f_pair += 2.0 * P2 * p * nm * (double)(e3 - b3);
     }
+    prof_mark(P, 4, st);
     k_final<<<std::min<int64_t>(((int64_t)nm * nm + 255) / 256, 4096), 256, 0, st>>>(
         P->Z.p, P->modes.p, p, nm, P->gamma.p);
     MG_LAUNCHED();
+    prof_mark(P, -1, st);
     launches += 1;
     P->flops_run = f_run;
     P->flops_x = f_x;
@@ -603,6 +635,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     P->launches = launches;
     // keep l0d alive until the stream drains
     MG_CUDA(cudaStreamSynchronize(st));
+    prof_collect(P);
 }
 
 void execute_rows(mg_plan* P, const std::vector<MgRow>& rows, cudaStream_t st) {

@@ -38,6 +38,15 @@ struct mg_plan {
     // stats of the last execute
     double flops_run = 0, flops_x = 0, flops_pair = 0;
     int64_t launches = 0;
+    // optional kernel timing: ms per family {weights, run, x, pair, final}, accumulated
+    bool profile = false;
+    double prof_ms[5] = {0, 0, 0, 0, 0};
+    std::vector<cudaEvent_t> prof_events;
+    std::vector<int> prof_tags;
+    size_t prof_used = 0;
+    ~mg_plan() {
+        for (auto e : prof_events) cudaEventDestroy(e);
+    }
     // host copies (for the direct/nonsep paths)
     std::vector<double> hC, hv;
 };

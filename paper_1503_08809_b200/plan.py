@@ -72,6 +72,14 @@ class GammaPlan:
         return {"flops_run": f[0].value, "flops_x": f[1].value, "flops_pair": f[2].value,
                 "launches": n.value}
 
+    def set_profile(self, on: bool = True):
+        nat.check(nat.lib().mg_plan_set_profile(self._h, int(bool(on))))
+
+    def kernel_ms(self) -> dict:
+        ms = np.zeros(5)
+        nat.check(nat.lib().mg_plan_kernel_ms(self._h, nat.ptr(ms)))
+        return dict(zip(("weights", "run", "x", "pair", "final"), ms.tolist()))
+
     def close(self):
         if self._h:
             nat.lib().mg_plan_destroy(self._h)

@@ -187,7 +187,8 @@ class TestGammaLarge:
     """Config-1 scale: flat-range partials vs the oracle on the same (GPU-built) q̃."""
 
     @pytest.fixture(scope="class")
-    def c1(self):
+    @staticmethod
+    def c1():
         from paper_1503_08809_b200 import build_qtilde
         hi = host_inputs("c1")
         C, qt = build_qtilde(hi)
