@@ -201,7 +201,7 @@ int mg_plan_set_profile(mg_plan* P, int on) {
 int mg_plan_kernel_ms(mg_plan* P, double* ms) {
     return guarded([&] {
         MG_REQUIRE(P && ms, "null argument");
-        for (int i = 0; i < 5; ++i) ms[i] = P->prof_ms[i];
+        for (int i = 0; i < MG_NPROF; ++i) ms[i] = P->prof_ms[i];
     });
 }
 

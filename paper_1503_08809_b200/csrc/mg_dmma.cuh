@@ -1,31 +1,39 @@
-// mg_dmma.cuh — FP64 tensor-core (DMMA) block GEMM with pluggable operand generators.
+// mg_dmma.cuh — FP64 tensor-core (DMMA) block GEMM with a cp.async multi-stage pipeline.
 //
 // Blackwell has no FP64 tcgen05 kind; FP64 tensor math is the legacy `mma.sync ... .f64`
 // path, which ptxas lowers to DMMA.8x8x4 on sm_100a (every f64 mma shape becomes a sequence
-// of 8x8x4 DMMAs, see profiles/r01_fp64_peak.txt).  Measured on this pool's B200: DMMA
-// 37.0 TFLOP/s vs DFMA 36.4 TFLOP/s, so the Γ contractions are written as DMMA GEMMs.
+// of 8x8x4 DMMAs; the NOP between consecutive DMMAs is ISA padding — the microbenchmark in
+// tools/fp64_peak.cu has the same pattern and reaches 37.0 of 37.2 nominal TFLOP/s).
 //
-// Tile: BM=128 x BN=128 x BK=16, 256 threads (8 warps as 2 x 4), warp tile 64 x 32 made of
-// 8 x 4 m8n8k4 fragments (64 FP64 accumulators per lane).  Operands are staged in shared
-// memory k-major (As[k][m], Bs[k][n]) with a +4 double row pad so the m8n8k4 fragment loads
-// (lane (g,t) reads [k0+t][m0+g]) are bank-conflict free.  Two smem stages; the next
-// k-tile's operands are produced into registers (by the loader functors, which may compute
-// them: pair products, weights, gathers) while the DMMAs of the current tile run.
+// Tile geometry is a template (Cfg): WARPS_M x WARPS_N warps, each owning FM x FN m8n8k4
+// fragments, so BM = 8*FM*WARPS_M, BN = 8*FN*WARPS_N.  Operand tiles live in shared memory
+// either k-major (X[k][m], row stride W+4) or m-major (X[m][k], row stride BK+4); both pads
+// keep the fragment reads (lane (g,t) reads element (m0+g, k0+t)) bank-conflict free and
+// rows 16-byte aligned for cp.async.  Tiles are streamed global->shared with cp.async
+// (16-byte chunks, zero-fill outside the matrix) through a STAGES-deep ring.  The A operand
+// may instead be produced per fragment by the producer from staged raw data (a_frag), which
+// is how the x contraction forms its pair products S_ab(x) without a shared-memory pass.
+// Fragments are double-buffered in registers across the k4 steps.
 #pragma once
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 namespace mg {
 
-constexpr int GB_M = 128;
-constexpr int GB_N = 128;
-constexpr int GB_K = 16;
-constexpr int GB_THREADS = 256;
-constexpr int GB_PAD = 4;
-constexpr int GB_LDA = GB_M + GB_PAD;  // row stride of As[k][*] in doubles
-constexpr int GB_LDB = GB_N + GB_PAD;
-constexpr int GB_STAGE = GB_K * (GB_LDA + GB_LDB);  // doubles per stage
-constexpr size_t GB_SMEM = 2 * GB_STAGE * sizeof(double);
+template <int WM_, int WN_, int FM_, int FN_>
+struct TileCfg {
+    static constexpr int WARPS_M = WM_, WARPS_N = WN_, FM = FM_, FN = FN_;
+    static constexpr int BM = 8 * FM_ * WM_, BN = 8 * FN_ * WN_;
+    static constexpr int THREADS = 32 * WM_ * WN_;
+};
+
+__host__ __device__ constexpr int ld_kmajor(int w) { return w + 4; }   // X[k][m]
+__host__ __device__ constexpr int ld_mmajor(int bk) { return bk + 4; }  // X[m][k]
+__host__ __device__ constexpr int tile_doubles(bool kmajor, int w, int bk) {
+    return kmajor ? bk * ld_kmajor(w) : w * ld_mmajor(bk);
+}
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
     asm volatile(
@@ -34,97 +42,160 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
         : "d"(a), "d"(b));
 }
 
-// Per-thread operand registers for one k-tile: 2048 elements / 256 threads = 8 each.
-struct Frag8 {
-    double v[8];
-};
-
-// Loader contract (A side; B identical with n in place of m):
-//   __device__ void load(int kt, Frag8& r) const;      // produce this thread's 8 elements
-//   __device__ void store(double* As, const Frag8& r) const;  // write them to As[k][m]
-// Two canonical thread->element maps are provided:
-//   "k-run":  m = tid % 128, k = (tid / 128) * 8 + i      (8 consecutive k of one m)
-//   "m-run":  k = tid / 16,  m = (tid % 16) * 8 + i       (8 consecutive m of one k)
-__device__ __forceinline__ void store_krun(double* S, int ld, const Frag8& r) {
-    int m = threadIdx.x & 127, k0 = (threadIdx.x >> 7) * 8;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) S[(k0 + i) * ld + m] = r.v[i];
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void store_mrun(double* S, int ld, const Frag8& r) {
-    int k = threadIdx.x >> 4, m0 = (threadIdx.x & 15) * 8;
-    double2* d = reinterpret_cast<double2*>(S + k * ld + m0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) d[i] = make_double2(r.v[2 * i], r.v[2 * i + 1]);
+// 16-byte async copy global->shared; src_bytes < 16 zero-fills the remainder.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Accumulator ownership: lane (g = lane/4, t = lane%4) of warp (wm, wn) holds, for
-// fragment (mi, ni), C[wm*64 + mi*8 + g][wn*32 + ni*8 + 2t + {0,1}].
-struct Acc {
-    double c[8][4][2];
-};
-
-// Core loop.  `ktiles` k-tiles of 16; A/B loaders as above; returns accumulators.
-template <class LA, class LB>
-__device__ __forceinline__ void gemm_mainloop(int ktiles, const LA& la, const LB& lb,
-                                              double* smem, Acc& acc) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, t = lane & 3;
-    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+// k-major tile: rows k in [0,BK), each W doubles from src_row(k) (nullptr -> zeros);
+// columns [w_valid, W) zero-filled.
+template <int BK, int W, int THREADS, class RowPtr>
+__device__ __forceinline__ void copy_kmajor(double* dst, RowPtr&& src_row, int w_valid) {
+    constexpr int CPR = W / 2, CH = BK * CPR;
+    static_assert(CH % THREADS == 0, "tile chunks must divide the thread count");
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
+    for (int i = 0; i < CH / THREADS; ++i) {
+        int c = threadIdx.x + i * THREADS;
+        int k = c / CPR, m = (c % CPR) * 2;
+        const double* s = src_row(k);
+        double* d = dst + k * ld_kmajor(W) + m;
+        int bytes = (s && m < w_valid) ? ((w_valid - m) >= 2 ? 16 : 8) : 0;
+        cp_async16(d, bytes ? s + m : d, bytes);
+    }
+}
+// m-major tile: rows m in [0,W), each BK doubles from src_row(m) (nullptr -> zeros);
+// k in [k_valid, BK) zero-filled.
+template <int BK, int W, int THREADS, class RowPtr>
+__device__ __forceinline__ void copy_mmajor(double* dst, RowPtr&& src_row, int k_valid) {
+    constexpr int CPR = BK / 2, CH = W * CPR;
+    static_assert(CH % THREADS == 0, "tile chunks must divide the thread count");
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
-    if (ktiles <= 0) return;
-
-    Frag8 ra, rb;
-    la.load(0, ra);
-    lb.load(0, rb);
-    la.store(smem, ra);
-    lb.store(smem + GB_K * GB_LDA, rb);
-    __syncthreads();
-
-    for (int kt = 0; kt < ktiles; ++kt) {
-        const double* As = smem + (kt & 1) * GB_STAGE;
-        const double* Bs = As + GB_K * GB_LDA;
-        const bool more = kt + 1 < ktiles;
-        if (more) {
-            la.load(kt + 1, ra);
-            lb.load(kt + 1, rb);
-        }
-#pragma unroll
-        for (int ks = 0; ks < GB_K / 4; ++ks) {
-            double a[8], b[4];
-            const double* Ak = As + (ks * 4 + t) * GB_LDA + wm + g;
-            const double* Bk = Bs + (ks * 4 + t) * GB_LDB + wn + g;
-#pragma unroll
-            for (int mi = 0; mi < 8; ++mi) a[mi] = Ak[mi * 8];
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) b[ni] = Bk[ni * 8];
-#pragma unroll
-            for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-                for (int ni = 0; ni < 4; ++ni) dmma884(acc.c[mi][ni], a[mi], b[ni]);
-        }
-        if (more) {
-            double* An = smem + ((kt + 1) & 1) * GB_STAGE;
-            la.store(An, ra);
-            lb.store(An + GB_K * GB_LDA, rb);
-        }
-        __syncthreads();
+    for (int i = 0; i < CH / THREADS; ++i) {
+        int c = threadIdx.x + i * THREADS;
+        int m = c / CPR, k = (c % CPR) * 2;
+        const double* s = src_row(m);
+        double* d = dst + m * ld_mmajor(BK) + k;
+        int bytes = (s && k < k_valid) ? ((k_valid - k) >= 2 ? 16 : 8) : 0;
+        cp_async16(d, bytes ? s + k : d, bytes);
     }
 }
 
-// Visit every accumulator element: f(m_local, n_local, value) with n in pairs (n, n+1).
-template <class F>
-__device__ __forceinline__ void acc_foreach_pair(const Acc& acc, F&& f) {
+template <class Cfg>
+struct Acc {
+    double c[Cfg::FM][Cfg::FN][2];
+};
+
+template <bool KMAJ, int W, int BK>
+__device__ __forceinline__ double frag_ld(const double* X, int k, int m) {
+    return KMAJ ? X[k * ld_kmajor(W) + m] : X[m * ld_mmajor(BK) + k];
+}
+
+// A-operand source of the pipeline.
+enum class ASrc { KMajor, MMajor, Raw };
+
+// Producer contract:
+//   __device__ void issue(int kt, double* As, double* Bs, double* raw) const;   // cp.async
+//   (ASrc::Raw only) __device__ double a_frag(const double* raw, int k, int fm) const;
+//     — value of A at (m = this lane's row of fragment fm, k) built from staged raw data.
+// Stage layout: [A tile (absent for Raw)][B tile][raw (kRaw doubles)].
+template <class Cfg, int BK, int STAGES, ASrc AS, bool BKM, int kRaw>
+struct Pipe {
+    static constexpr int SA = AS == ASrc::Raw ? 0 : tile_doubles(AS == ASrc::KMajor, Cfg::BM, BK);
+    static constexpr int SB = tile_doubles(BKM, Cfg::BN, BK);
+    static constexpr int SS = SA + SB + kRaw;
+    static constexpr size_t smem_bytes = (size_t)STAGES * SS * sizeof(double);
+
+    template <class Prod>
+    __device__ static void run(int ktiles, const Prod& prod, double* smem, Acc<Cfg>& acc) {
+        constexpr int FM = Cfg::FM, FN = Cfg::FN;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int g = lane >> 2, t = lane & 3;
+        const int wm = (warp / Cfg::WARPS_N) * (8 * FM), wn = (warp % Cfg::WARPS_N) * (8 * FN);
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
+        if (ktiles <= 0) return;
+
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < ktiles) {
+                double* st = smem + s * SS;
+                prod.issue(s, st, st + SA, st + SA + SB);
+            }
+            cp_async_commit();
+        }
+
+        for (int kt = 0; kt < ktiles; ++kt) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            const double* st = smem + (kt % STAGES) * SS;
+            const double* As = st;
+            const double* Bs = st + SA;
+            const double* raw = st + SA + SB;
+            {   // refill the stage consumed in iteration kt-1
+                int nk = kt + STAGES - 1;
+                if (nk < ktiles) {
+                    double* ns = smem + (nk % STAGES) * SS;
+                    prod.issue(nk, ns, ns + SA, ns + SA + SB);
+                }
+                cp_async_commit();
+            }
+            double a[2][FM], b[2][FN];
+            auto load_frags = [&](int buf, int k) {
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi) {
+                    if constexpr (AS == ASrc::Raw)
+                        a[buf][mi] = prod.a_frag(raw, k, mi);
+                    else
+                        a[buf][mi] = frag_ld<AS == ASrc::KMajor, Cfg::BM, BK>(As, k, wm + mi * 8 + g);
+                }
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni)
+                    b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g);
+            };
+            load_frags(0, t);
+#pragma unroll
+            for (int ks = 0; ks < BK / 4; ++ks) {
+                const int cur = ks & 1;
+                if (ks + 1 < BK / 4) load_frags(cur ^ 1, (ks + 1) * 4 + t);
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < FN; ++ni) dmma884(acc.c[mi][ni], a[cur][mi], b[cur][ni]);
+            }
+        }
+        cp_async_wait<0>();
+    }
+};
+
+// Visit every accumulator element: f(m_local, n_local, v(n), v(n+1)).
+template <class Cfg, class F>
+__device__ __forceinline__ void acc_foreach_pair(const Acc<Cfg>& acc, F&& f) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+    const int wm = (warp / Cfg::WARPS_N) * (8 * Cfg::FM), wn = (warp % Cfg::WARPS_N) * (8 * Cfg::FN);
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
+    for (int mi = 0; mi < Cfg::FM; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < Cfg::FN; ++ni)
             f(wm + mi * 8 + g, wn + ni * 8 + 2 * t, acc.c[mi][ni][0], acc.c[mi][ni][1]);
+}
+
+// Lane's row (within the CTA tile) of fragment fm: wm + 8 fm + g.
+template <class Cfg>
+__device__ __forceinline__ int frag_row(int fm) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    return (warp / Cfg::WARPS_N) * (8 * Cfg::FM) + fm * 8 + (lane >> 2);
 }
 
 }  // namespace mg

@@ -52,22 +52,8 @@ __global__ void k_transpose_qt(const double* __restrict__ qt, const double* __re
 }
 
 // ------------------------------------------------------------------------------------------
-// K0: per-row weight windows  ZT[off(row) + j - jlo] = zm(l1(j), l2, l3)
+// K0: explicit-triple weights (only for arbitrary domains): ZT pre-zeroed, zm scattered
 // ------------------------------------------------------------------------------------------
-__global__ void k_row_weights(const MgRow* __restrict__ rows, const int64_t* __restrict__ zoff,
-                              int64_t zbase, int l_min, const int* __restrict__ l0,
-                              const double* __restrict__ C, const double* __restrict__ v,
-                              const double* __restrict__ lf, int mode,
-                              double* __restrict__ ZT) {
-    MgRow r = rows[blockIdx.x];
-    int64_t o = zoff[blockIdx.x] - zbase;
-    for (int j = r.jlo + threadIdx.x; j <= r.jhi; j += blockDim.x) {
-        int l1 = l0[r.par] + 2 * j;
-        ZT[o + j - r.jlo] = zm_weight(mode, l1, r.l2, r.l3, C, v, l_min, lf);
-    }
-}
-
-// explicit-triple variant: ZT pre-zeroed, then zm of listed triples scattered (x count)
 __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
                                   const int32_t* __restrict__ t3, const int64_t* __restrict__ pos,
                                   const double* __restrict__ dup, int64_t n, int64_t zbase,
@@ -80,82 +66,106 @@ __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t*
 }
 
 // ------------------------------------------------------------------------------------------
-// K1: run contraction  H[(r,c)][(c',x)] = Σ_j A[(r,c)][j] WQT[cls+j][(c',x)]
+// K1a: A panels of the run contraction, one per M-tile, k-major [jl][slot]:
+//   panel[jl][slot=(r,c)] = zm(l1(j), l2_r, l3_r) q_c(l1(j))  (0 outside row r's window)
 // ------------------------------------------------------------------------------------------
-struct RunA {  // A[slot][j] = ZT * q[c][l1], k-run map
-    const double* zt;   // row's ZT window base (valid if ok)
-    const double* qc;   // q[c][*] shifted so that qc[l1] is q_c(l1)
-    int jlo, jhi, jt0, l0;
-    bool ok;
-    __device__ void load(int kt, Frag8& r) const {
-        int k0 = (threadIdx.x >> 7) * 8;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            int j = jt0 + kt * GB_K + k0 + i;
-            bool in = ok && j >= jlo && j <= jhi;
-            r.v[i] = in ? zt[j - jlo] * qc[l0 + 2 * j] : 0.0;
-        }
-    }
-    __device__ void store(double* S, const Frag8& r) const { store_krun(S, GB_LDA, r); }
-};
-struct RunB {  // B[j][n] = WQT[cls+j][n], m-run map, n contiguous
-    const double* base;  // WQT + cls*ldb
-    int64_t ldb;         // p * NxP
-    int jt0, jhi, n0;
-    __device__ void load(int kt, Frag8& r) const {
-        int k = threadIdx.x >> 4, n = n0 + (threadIdx.x & 15) * 8;
-        int j = jt0 + kt * GB_K + k;
-        if (j <= jhi && n < ldb) {
-            const double2* s = reinterpret_cast<const double2*>(base + (int64_t)j * ldb + n);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                double2 d = __ldg(s + i);
-                r.v[2 * i] = d.x;
-                r.v[2 * i + 1] = d.y;
+constexpr int RUN_BK = 32, RUN_ST = 3;
+constexpr int X_BK = 32, X_ST = 2;
+constexpr int PAIR_BK = 32, PAIR_ST = 3;
+using Cfg128 = TileCfg<2, 4, 8, 4>;  // 128 x 128, 8 warps, 64 accumulators per lane
+using CfgX = TileCfg<4, 2, 4, 5>;    // 128 x 80, 8 warps, 40 accumulators per lane
+using RunPipe = Pipe<Cfg128, RUN_BK, RUN_ST, ASrc::KMajor, true, 0>;
+using PairPipe = Pipe<Cfg128, PAIR_BK, PAIR_ST, ASrc::KMajor, true, 0>;
+constexpr int GB_M = 128;
+
+constexpr int PANEL_THREADS = 256;
+constexpr int PANEL_JC = 64;  // j values per shared-memory weight chunk
+
+__global__ void __launch_bounds__(PANEL_THREADS)
+k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
+             const int64_t* __restrict__ poff, const int64_t* __restrict__ zoff, int64_t zbase,
+             const double* __restrict__ ZT, const int* __restrict__ l0,
+             const double* __restrict__ q, int L, int l_min, int p, int P8,
+             const double* __restrict__ C, const double* __restrict__ v,
+             const double* __restrict__ lf, int mode, double* __restrict__ panel) {
+    __shared__ double zs[GB_M / 8][PANEL_JC];  // zm of (row, j) for the current j chunk
+    const MgTile tl = tiles[blockIdx.x];
+    const int kt = (tl.jhi - tl.jlo + RUN_BK) / RUN_BK * RUN_BK;
+    double* out = panel + poff[blockIdx.x];
+    const int nrz = tl.nrows;  // <= 16 rows per tile
+    for (int jc = 0; jc < kt; jc += PANEL_JC) {
+        // 1) each (row, j) weight once
+        for (int e = threadIdx.x; e < nrz * PANEL_JC; e += PANEL_THREADS) {
+            const int rr = e / PANEL_JC, jl = e % PANEL_JC;
+            const int j = tl.jlo + jc + jl;
+            const MgRow rw = rows[tl.row0 + rr];
+            double z = 0.0;
+            if (jc + jl < kt && j >= rw.jlo && j <= rw.jhi) {
+                if (ZT) {
+                    z = ZT[zoff[tl.row0 + rr] - zbase + (j - rw.jlo)];
+                } else {
+                    z = zm_weight(mode, l0[rw.par] + 2 * j, rw.l2, rw.l3, C, v, l_min, lf);
+                }
             }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) r.v[i] = 0.0;
+            zs[rr][jl] = z;
         }
+        __syncthreads();
+        // 2) panel[j][slot] = zm(row(slot), j) * q_c(slot)(l1(j)), slot-contiguous stores
+        const int par = rows[tl.row0].par;
+        for (int e = threadIdx.x; e < PANEL_JC * GB_M; e += PANEL_THREADS) {
+            const int jl = e / GB_M, slot = e % GB_M;
+            if (jc + jl >= kt) break;
+            const int rr = slot / P8, c = slot - rr * P8;
+            double val = 0.0;
+            if (rr < nrz && c < p) {
+                const int l1 = l0[par] + 2 * (tl.jlo + jc + jl);
+                const double z = zs[rr][jl];
+                if (z != 0.0) val = z * q[(int64_t)c * L + (l1 - l_min)];
+            }
+            out[(int64_t)(jc + jl) * GB_M + slot] = val;
+        }
+        __syncthreads();
     }
-    __device__ void store(double* S, const Frag8& r) const { store_mrun(S, GB_LDB, r); }
+}
+
+// ------------------------------------------------------------------------------------------
+// K1: run contraction  H[(r,c)][(c',x)] = Σ_j panel[j][(r,c)] WQT[cls+j][(c',x)]
+// ------------------------------------------------------------------------------------------
+struct RunProd {
+    const double* panel;  // this tile's panel
+    const double* wqt;    // WQT + cls*ldb + n0
+    int64_t ldb;
+    int jlo, jhi, n_valid;
+    __device__ void issue(int kt, double* As, double* Bs, double*) const {
+        copy_kmajor<RUN_BK, 128, 256>(
+            As, [&](int k) { return panel + (int64_t)(kt * RUN_BK + k) * GB_M; }, GB_M);
+        copy_kmajor<RUN_BK, 128, 256>(Bs, [&](int k) -> const double* {
+            int j = jlo + kt * RUN_BK + k;
+            return j <= jhi ? wqt + (int64_t)j * ldb : nullptr;
+        }, n_valid);
+    }
 };
 
-__global__ void __launch_bounds__(GB_THREADS, 1)
-k_run_contract(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
-               const int64_t* __restrict__ zoff, int64_t zbase, int row_base,
-               const double* __restrict__ ZT, const double* __restrict__ q,
-               const double* __restrict__ WQT, int p, int P8, int NxP, int L, int l_min,
-               int l0e, int l0o, int cbase0, int cbase1, double* __restrict__ H) {
+__global__ void __launch_bounds__(256, 1)
+k_run_contract(const MgTile* __restrict__ tiles, const int64_t* __restrict__ poff,
+               const double* __restrict__ panel, int row_base, const MgRow* __restrict__ rows,
+               const double* __restrict__ WQT, int p, int P8, int NxP, int cbase0, int cbase1,
+               double* __restrict__ H) {
     extern __shared__ __align__(16) double smem[];
     const MgTile tl = tiles[blockIdx.y];
-    const int n0 = blockIdx.x * GB_N;
+    const int n0 = blockIdx.x * Cfg128::BN;
     const int64_t ldb = (int64_t)p * NxP;
-    const MgRow r0 = rows[tl.row0];
-    const int par = r0.par;
-    const int l0 = par ? l0o : l0e;
-    RunA la;
-    {
-        int m = threadIdx.x & 127;
-        int rr = m / P8, c = m - rr * P8;
-        la.ok = rr < tl.nrows && c < p;
-        MgRow rw = la.ok ? rows[tl.row0 + rr] : r0;
-        la.zt = ZT + (zoff[tl.row0 + (la.ok ? rr : 0)] - zbase);
-        la.qc = q + (int64_t)(la.ok ? c : 0) * L - l_min;
-        la.jlo = rw.jlo;
-        la.jhi = rw.jhi;
-        la.jt0 = tl.jlo;
-        la.l0 = l0;
-    }
-    RunB lb;
-    lb.base = WQT + (int64_t)(par ? cbase1 : cbase0) * ldb;
-    lb.ldb = ldb;
-    lb.jt0 = tl.jlo;
-    lb.jhi = tl.jhi;
-    lb.n0 = n0;
-    Acc acc;
-    gemm_mainloop((tl.jhi - tl.jlo + GB_K) / GB_K, la, lb, smem, acc);
-    acc_foreach_pair(acc, [&](int m, int n, double v0, double v1) {
+    const int par = rows[tl.row0].par;
+    RunProd pr;
+    pr.panel = panel + poff[blockIdx.y];
+    pr.wqt = WQT + (int64_t)(par ? cbase1 : cbase0) * ldb + n0;
+    pr.ldb = ldb;
+    pr.jlo = tl.jlo;
+    pr.jhi = tl.jhi;
+    pr.n_valid = (int)(ldb - n0 < Cfg128::BN ? ldb - n0 : Cfg128::BN);
+    Acc<Cfg128> acc;
+    RunPipe::run((tl.jhi - tl.jlo + RUN_BK) / RUN_BK, pr, smem, acc);
+    acc_foreach_pair<Cfg128>(acc, [&](int m, int n, double v0, double v1) {
         int rr = m / P8, c = m - rr * P8;
         int gn = n0 + n;
         if (rr < tl.nrows && c < p && gn < ldb) {
@@ -166,7 +176,9 @@ k_run_contract(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
 }
 
 // ------------------------------------------------------------------------------------------
-// K2: x contraction  G[r][ab][(c,c')] = Σ_x S_ab(x) H[r][(c,c')][x]
+// K2: x contraction  G[r][(c,c')][ab] = Σ_x S_ab(x) H[r][(c,c')][x]
+//   A = S (pairs x x, built in shared memory from the staged q̃(l2), q̃(l3) slices),
+//   B = H row (m-major, streamed by cp.async).
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void pair_of(int pr, int& a, int& b) {
     int bb = (int)((sqrt(8.0 * pr + 1.0) - 1.0) * 0.5);
@@ -179,182 +191,195 @@ __device__ __forceinline__ int pair_idx(int a, int b) {  // a <= b
     return b * (b + 1) / 2 + a;
 }
 
-struct XA {  // S[pair][x], k-run map
-    const double *r2a, *r2b, *r3a, *r3b;
-    bool ok;
-    __device__ void load(int kt, Frag8& r) const {
-        int x0 = kt * GB_K + (threadIdx.x >> 7) * 8;
-        if (ok) {
-#pragma unroll
-            for (int i = 0; i < 8; i += 2) {
-                double2 a2 = *reinterpret_cast<const double2*>(r2a + x0 + i);
-                double2 b2 = *reinterpret_cast<const double2*>(r2b + x0 + i);
-                double2 a3 = *reinterpret_cast<const double2*>(r3a + x0 + i);
-                double2 b3 = *reinterpret_cast<const double2*>(r3b + x0 + i);
-                r.v[i] = a2.x * b3.x + b2.x * a3.x;
-                r.v[i + 1] = a2.y * b3.y + b2.y * a3.y;
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) r.v[i] = 0.0;
+// raw row stride: 16-byte aligned and = 4 (mod 16) doubles, so the fragment-level reads of
+// rows a, a+1, a+2, a+3 (lanes g) at k0+t land in disjoint 8-bank windows
+constexpr int X_LDR = X_BK + 4;
+constexpr int X_ZROW = 32;              // all-zero row (pairs past P2 point here)
+constexpr int X_RAW = 2 * 33 * X_LDR;   // q̃(l2)[c][k] rows 0..32, then q̃(l3)[c][k] rows 0..32
+using XPipe = Pipe<CfgX, X_BK, X_ST, ASrc::Raw, false, X_RAW>;
+
+struct XProd {
+    const double* q2;  // QT[l2] (p x NxP)
+    const double* q3;  // QT[l3]
+    const double* h;   // H row (pp x NxP)
+    int p, NxP, pp, n0;
+    int off[CfgX::FM];  // per fragment: a*X_LDR | (b*X_LDR) << 16 of this lane's pair
+    __device__ void issue(int kt, double*, double* Bs, double* raw) const {
+        const int cpr = X_BK / 2;  // chunks per q̃ row slice
+        for (int c = threadIdx.x; c < 2 * p * cpr; c += CfgX::THREADS) {
+            int which = c / (p * cpr), rem = c % (p * cpr);
+            int cc = rem / cpr, k = (rem % cpr) * 2;
+            const double* src = (which ? q3 : q2) + (int64_t)cc * NxP + kt * X_BK + k;
+            cp_async16(raw + (which * 33 + cc) * X_LDR + k, src, 16);
         }
+        copy_mmajor<X_BK, CfgX::BN, CfgX::THREADS>(Bs, [&](int m) -> const double* {
+            int cc = n0 + m;
+            return cc < pp ? h + (int64_t)cc * NxP + kt * X_BK : nullptr;
+        }, X_BK);
     }
-    __device__ void store(double* S, const Frag8& r) const { store_krun(S, GB_LDA, r); }
-};
-struct XB {  // H[r][cc'][x], k-run map
-    const double* h;
-    bool ok;
-    __device__ void load(int kt, Frag8& r) const {
-        int x0 = kt * GB_K + (threadIdx.x >> 7) * 8;
-        if (ok) {
-            const double2* s = reinterpret_cast<const double2*>(h + x0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                double2 d = s[i];
-                r.v[2 * i] = d.x;
-                r.v[2 * i + 1] = d.y;
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) r.v[i] = 0.0;
-        }
+    // S_ab(x_k) = q̃_a(x,l2) q̃_b(x,l3) + q̃_b(x,l2) q̃_a(x,l3)   (branch-free: pads read zeros)
+    __device__ double a_frag(const double* raw, int k, int fm) const {
+        const int o = off[fm];
+        const int oa = o & 0xffff, ob = o >> 16;
+        const double* r3 = raw + 33 * X_LDR;
+        return raw[oa + k] * r3[ob + k] + raw[ob + k] * r3[oa + k];
     }
-    __device__ void store(double* S, const Frag8& r) const { store_krun(S, GB_LDB, r); }
 };
 
-__global__ void __launch_bounds__(GB_THREADS, 1)
+#ifndef MG_X_MINB
+#define MG_X_MINB 2
+#endif
+__global__ void __launch_bounds__(CfgX::THREADS, MG_X_MINB)
 k_x_contract(const MgRow* __restrict__ rows, int row_b1, int row_b3,
              const double* __restrict__ QT, const double* __restrict__ H, int p, int P2,
              int NxP, int l_min, double* __restrict__ G) {
     extern __shared__ __align__(16) double smem[];
     const int r = blockIdx.z;  // row within the K1/K2 batch
     const MgRow rw = rows[row_b1 + r];
-    const int m0 = blockIdx.y * GB_M, n0 = blockIdx.x * GB_N;
+    const int m0 = blockIdx.y * CfgX::BM, n0 = blockIdx.x * CfgX::BN;
     const int pp = p * p;
-    XA la;
-    {
-        int pr = m0 + (threadIdx.x & 127);
-        la.ok = pr < P2;
-        int a = 0, b = 0;
-        if (la.ok) pair_of(pr, a, b);
-        const double* q2 = QT + (int64_t)(rw.l2 - l_min) * p * NxP;
-        const double* q3 = QT + (int64_t)(rw.l3 - l_min) * p * NxP;
-        la.r2a = q2 + (int64_t)a * NxP;
-        la.r2b = q2 + (int64_t)b * NxP;
-        la.r3a = q3 + (int64_t)a * NxP;
-        la.r3b = q3 + (int64_t)b * NxP;
+    XProd pr;
+    pr.q2 = QT + (int64_t)(rw.l2 - l_min) * p * NxP;
+    pr.q3 = QT + (int64_t)(rw.l3 - l_min) * p * NxP;
+    pr.h = H + (int64_t)r * pp * NxP;
+    pr.p = p;
+    pr.NxP = NxP;
+    pr.pp = pp;
+    pr.n0 = n0;
+#pragma unroll
+    for (int fm = 0; fm < CfgX::FM; ++fm) {
+        int prr = m0 + frag_row<CfgX>(fm);
+        if (prr < P2) {
+            int a, b;
+            pair_of(prr, a, b);
+            pr.off[fm] = a * X_LDR | ((b * X_LDR) << 16);
+        } else {
+            pr.off[fm] = X_ZROW * X_LDR | ((X_ZROW * X_LDR) << 16);
+        }
     }
-    XB lb;
-    {
-        int cc = n0 + (threadIdx.x & 127);
-        lb.ok = cc < pp;
-        lb.h = H + ((int64_t)r * pp + (lb.ok ? cc : 0)) * NxP;
+    for (int i = threadIdx.x; i < X_ST * X_LDR; i += CfgX::THREADS) {  // zero rows, all stages
+        double* st = smem + (i / X_LDR) * XPipe::SS + XPipe::SA + XPipe::SB;
+        st[X_ZROW * X_LDR + i % X_LDR] = 0.0;
+        st[(33 + X_ZROW) * X_LDR + i % X_LDR] = 0.0;
     }
-    Acc acc;
-    gemm_mainloop(NxP / GB_K, la, lb, smem, acc);
-    double* Gr = G + (int64_t)(row_b1 + r - row_b3) * P2 * pp;
-    acc_foreach_pair(acc, [&](int m, int n, double v0, double v1) {
-        int pr = m0 + m, cc = n0 + n;
-        if (pr < P2) {
-            if (cc < pp) Gr[(int64_t)pr * pp + cc] = v0;
-            if (cc + 1 < pp) Gr[(int64_t)pr * pp + cc + 1] = v1;
+    Acc<CfgX> acc;
+    XPipe::run(NxP / X_BK, pr, smem, acc);
+    double* Gr = G + (int64_t)(row_b1 + r - row_b3) * pp * P2;
+    acc_foreach_pair<CfgX>(acc, [&](int m, int n, double v0, double v1) {
+        int prr = m0 + m, cc = n0 + n;
+        if (prr < P2) {
+            if (cc < pp) Gr[(int64_t)cc * P2 + prr] = v0;
+            if (cc + 1 < pp) Gr[(int64_t)(cc + 1) * P2 + prr] = v1;
         }
     });
 }
 
 // ------------------------------------------------------------------------------------------
-// K3: pair contraction over rows  Z[ab][(c,n')] += Σ_r Sq_ab(r) R_r[c][n']
+// K2b: gather  R[r][c*nm + n'] = G[r][c,k'][i'j'] + G[r][c,j'][i'k'] + G[r][c,i'][j'k']
+//      and pair sums Sq[r][ab] = q_a(l2) q_b(l3) + q_b(l2) q_a(l3)
 // ------------------------------------------------------------------------------------------
-struct PA {  // Sq[pair][row], k-run map
-    const MgRow* rows;
-    const double *qa, *qb;  // q[a][*], q[b][*] shifted by -l_min
-    int nrows;
-    bool ok;
-    __device__ void load(int kt, Frag8& r) const {
-        int k0 = kt * GB_K + (threadIdx.x >> 7) * 8;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            int rr = k0 + i;
-            if (ok && rr < nrows) {
-                MgRow w = rows[rr];
-                r.v[i] = qa[w.l2] * qb[w.l3] + qb[w.l2] * qa[w.l3];
-            } else {
-                r.v[i] = 0.0;
+__global__ void k_gather(const MgRow* __restrict__ rows, const double* __restrict__ G,
+                         const int* __restrict__ modes, const double* __restrict__ q, int L,
+                         int l_min, int p, int P2, int nm, int64_t ldr, int ldq,
+                         double* __restrict__ R, double* __restrict__ Sq) {
+    const int r = blockIdx.y;
+    const int pp = p * p;
+    const double* Gr = G + (int64_t)r * pp * P2;
+    const int ncols = p * nm;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < ncols;
+         idx += gridDim.x * blockDim.x) {
+        int c = idx / nm, np = idx - c * nm;
+        int a = modes[3 * np], b = modes[3 * np + 1], d = modes[3 * np + 2];
+        int cp = c * p;
+        R[(int64_t)r * ldr + idx] = Gr[(int64_t)(cp + d) * P2 + pair_idx(a, b)] +
+                                    Gr[(int64_t)(cp + b) * P2 + pair_idx(a, d)] +
+                                    Gr[(int64_t)(cp + a) * P2 + pair_idx(b, d)];
+    }
+    if (blockIdx.x == 0) {
+        const MgRow w = rows[r];
+        for (int pr = threadIdx.x; pr < ldq; pr += blockDim.x) {
+            double s = 0.0;
+            if (pr < P2) {
+                int a, b;
+                pair_of(pr, a, b);
+                const double* qa = q + (int64_t)a * L - l_min;
+                const double* qb = q + (int64_t)b * L - l_min;
+                s = qa[w.l2] * qb[w.l3] + qb[w.l2] * qa[w.l3];
             }
+            Sq[(int64_t)r * ldq + pr] = s;
         }
     }
-    __device__ void store(double* S, const Frag8& r) const { store_krun(S, GB_LDA, r); }
-};
-struct PB {  // R[row][n] gathered from G, m-run map
-    const double* G;
-    const int* modes;
-    int p, P2, nm, nrows, ncols, n0;
-    __device__ void load(int kt, Frag8& r) const {
-        int rr = kt * GB_K + (threadIdx.x >> 4);
-        int nb = n0 + (threadIdx.x & 15) * 8;
-        const int pp = p * p;
-        const double* Gr = G + (int64_t)rr * P2 * pp;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            int n = nb + i;
-            double val = 0.0;
-            if (rr < nrows && n < ncols) {
-                int c = n / nm, np = n - c * nm;
-                int a = modes[3 * np], b = modes[3 * np + 1], d = modes[3 * np + 2];
-                int cp = c * p;
-                val = Gr[(int64_t)pair_idx(a, b) * pp + cp + d] +
-                      Gr[(int64_t)pair_idx(a, d) * pp + cp + b] +
-                      Gr[(int64_t)pair_idx(b, d) * pp + cp + a];
-            }
-            r.v[i] = val;
-        }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3: pair contraction over rows  Z_s[ab][(c,n')] += Σ_{r in split s} Sq[r][ab] R[r][(c,n')]
+// ------------------------------------------------------------------------------------------
+struct PairProd {
+    const double* sq;  // Sq + r0*ldq + m0
+    const double* rr;  // R + r0*ldr + n0
+    int ldq;
+    int64_t ldr;
+    int nr, m_valid, n_valid;
+    __device__ void issue(int kt, double* As, double* Bs, double*) const {
+        copy_kmajor<PAIR_BK, 128, 256>(As, [&](int k) -> const double* {
+            int r = kt * PAIR_BK + k;
+            return r < nr ? sq + (int64_t)r * ldq : nullptr;
+        }, m_valid);
+        copy_kmajor<PAIR_BK, 128, 256>(Bs, [&](int k) -> const double* {
+            int r = kt * PAIR_BK + k;
+            return r < nr ? rr + (int64_t)r * ldr : nullptr;
+        }, n_valid);
     }
-    __device__ void store(double* S, const Frag8& r) const { store_mrun(S, GB_LDB, r); }
 };
 
-__global__ void __launch_bounds__(GB_THREADS, 1)
-k_pair_contract(const MgRow* __restrict__ rows, int nrows, const double* __restrict__ q,
-                const double* __restrict__ G, const int* __restrict__ modes, int p, int P2,
-                int nm, int L, int l_min, double* __restrict__ Z) {
+__global__ void __launch_bounds__(256, 1)
+k_pair_contract(const double* __restrict__ Sq, int ldq, const double* __restrict__ R,
+                int64_t ldr, int nrows, int per_split, int P2, int ncols, int64_t zsplit,
+                double* __restrict__ Z) {
     extern __shared__ __align__(16) double smem[];
-    const int m0 = blockIdx.y * GB_M, n0 = blockIdx.x * GB_N;
-    const int ncols = p * nm;
-    PA la;
-    {
-        int pr = m0 + (threadIdx.x & 127);
-        la.ok = pr < P2;
-        int a = 0, b = 0;
-        if (la.ok) pair_of(pr, a, b);
-        la.qa = q + (int64_t)a * L - l_min;
-        la.qb = q + (int64_t)b * L - l_min;
-        la.rows = rows;
-        la.nrows = nrows;
-    }
-    PB lb{G, modes, p, P2, nm, nrows, ncols, n0};
-    Acc acc;
-    gemm_mainloop((nrows + GB_K - 1) / GB_K, la, lb, smem, acc);
-    acc_foreach_pair(acc, [&](int m, int n, double v0, double v1) {
-        int pr = m0 + m, c = n0 + n;
-        if (pr < P2) {
-            double* z = Z + (int64_t)pr * ncols;
+    const int m0 = blockIdx.y * Cfg128::BM, n0 = blockIdx.x * Cfg128::BN;
+    const int s = blockIdx.z;
+    const int r0 = s * per_split;
+    const int nr = min(per_split, nrows - r0);
+    if (nr <= 0) return;
+    PairProd pr;
+    pr.sq = Sq + (int64_t)r0 * ldq + m0;
+    pr.rr = R + (int64_t)r0 * ldr + n0;
+    pr.ldq = ldq;
+    pr.ldr = ldr;
+    pr.nr = nr;
+    pr.m_valid = min(Cfg128::BM, P2 - m0);
+    pr.n_valid = min(Cfg128::BN, ncols - n0);
+    Acc<Cfg128> acc;
+    PairPipe::run((nr + PAIR_BK - 1) / PAIR_BK, pr, smem, acc);
+    double* Zs = Z + s * zsplit;
+    acc_foreach_pair<Cfg128>(acc, [&](int m, int n, double v0, double v1) {
+        int prr = m0 + m, c = n0 + n;
+        if (prr < P2) {
+            double* z = Zs + (int64_t)prr * ncols;
             if (c < ncols) z[c] += v0;
             if (c + 1 < ncols) z[c + 1] += v1;
         }
     });
 }
 
-// Γ[(ijk)][n'] = Z[ij][k][n'] + Z[ik][j][n'] + Z[jk][i][n']
-__global__ void k_final(const double* __restrict__ Z, const int* __restrict__ modes, int p,
-                        int nm, double* __restrict__ gamma) {
+// Γ[(ijk)][n'] = Σ_s Z_s[ij][k][n'] + Z_s[ik][j][n'] + Z_s[jk][i][n']   (splits in order)
+__global__ void k_final(const double* __restrict__ Z, int nsplit, int64_t zsplit,
+                        const int* __restrict__ modes, int p, int nm, double* __restrict__ gamma) {
     int64_t total = (int64_t)nm * nm;
     const int64_t ncols = (int64_t)p * nm;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         int n = (int)(i / nm), np = (int)(i % nm);
         int a = modes[3 * n], b = modes[3 * n + 1], d = modes[3 * n + 2];
-        gamma[i] = Z[pair_idx(a, b) * ncols + (int64_t)d * nm + np] +
-                   Z[pair_idx(a, d) * ncols + (int64_t)b * nm + np] +
-                   Z[pair_idx(b, d) * ncols + (int64_t)a * nm + np];
+        double acc = 0.0;
+        for (int s = 0; s < nsplit; ++s) {
+            const double* Zs = Z + s * zsplit;
+            acc += Zs[pair_idx(a, b) * ncols + (int64_t)d * nm + np] +
+                   Zs[pair_idx(a, d) * ncols + (int64_t)b * nm + np] +
+                   Zs[pair_idx(b, d) * ncols + (int64_t)a * nm + np];
+        }
+        gamma[i] = acc;
     }
 }
 
@@ -375,7 +400,7 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
     MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
     MG_REQUIRE(p >= 1 && Nx >= 1 && n >= 1, "p, Nx, n must be >= 1");
     MG_REQUIRE(h2_mode == MG_H2_GOSPER || h2_mode == MG_H2_EXACT, "unknown h2_mode");
-    MG_REQUIRE(p <= 64, "p_max > 64 not supported");
+    MG_REQUIRE(p <= 32, "p_max > 32 not supported");
     const int L = l_max - l_min + 1;
     for (int i = 0; i < L; ++i) {
         MG_REQUIRE(C[i] > 0, "power spectrum C_l must be strictly positive");
@@ -389,7 +414,7 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
     }
     P->p = p; P->Nx = Nx; P->nm = n; P->l_min = l_min; P->l_max = l_max; P->L = L;
     P->h2_mode = h2_mode;
-    P->NxP = (int)round_up(Nx, GB_K);
+    P->NxP = (int)round_up(Nx, X_BK);
     P->P2 = p * (p + 1) / 2;
     P->P8 = (int)round_up(p, 8);
     P->rpt = std::max(1, GB_M / P->P8);
@@ -499,7 +524,7 @@ static void prof_collect(mg_plan* P) {
         float ms = 0.f;
         MG_CUDA(cudaEventElapsedTime(&ms, P->prof_events[i], P->prof_events[i + 1]));
         int tag = P->prof_tags[i];
-        if (tag >= 0 && tag < 5) P->prof_ms[tag] += ms;
+        if (tag >= 0 && tag < MG_NPROF) P->prof_ms[tag] += ms;
     }
     P->prof_used = 0;
     P->prof_tags.clear();
@@ -514,13 +539,21 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     const int64_t nrows = (int64_t)hrows.size();
     if (!P->nb1) choose_batches(P);
     const int nb1 = P->nb1, nb3 = P->nb3;
+    const int pp = p * p;
+    const int ncols = p * nm;
+    const int64_t ldr = round_up(ncols, 2);
+    const int ldq = (int)round_up(P2, 2);
 
-    // tiles: consecutive rows of one (l2, par) group, at most rpt per tile, per nb1-batch
+    // tiles: consecutive rows of one (l2, par) group, at most rpt per tile, per nb1-batch;
+    // each tile owns a k-major A panel of round_up(window, RUN_BK) x 128 doubles.
     std::vector<MgTile> tiles;
-    std::vector<int> tile_first;  // per nb1 batch
+    std::vector<int64_t> poff;      // panel offset of each tile, relative to its batch
+    std::vector<int> tile_first;    // per nb1 batch
+    std::vector<int64_t> panel_len; // per nb1 batch
     for (int64_t b1 = 0; b1 < nrows; b1 += nb1) {
         int64_t e1 = std::min<int64_t>(b1 + nb1, nrows);
         tile_first.push_back((int)tiles.size());
+        int64_t off = 0;
         int64_t i = b1;
         while (i < e1) {
             MgTile t;
@@ -536,33 +569,57 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                 ++i;
             }
             tiles.push_back(t);
+            poff.push_back(off);
+            off += round_up(t.jhi - t.jlo + 1, RUN_BK) * GB_M;
         }
+        panel_len.push_back(off);
     }
     tile_first.push_back((int)tiles.size());
 
     P->rows.upload(hrows.data(), hrows.size(), st);
     P->zoff.upload(hzoff.data(), hzoff.size(), st);
     P->tiles.upload(tiles.data(), tiles.size(), st);
-    int64_t maxzt = 0;
-    for (int64_t b1 = 0; b1 < nrows; b1 += nb1) {
-        int64_t e1 = std::min<int64_t>(b1 + nb1, nrows);
+    P->poff.upload(poff.data(), poff.size(), st);
+    int64_t maxzt = 1, maxpanel = 1;
+    for (size_t bi = 0; bi + 1 < tile_first.size(); ++bi) {
+        int64_t b1 = bi * (int64_t)nb1, e1 = std::min<int64_t>(b1 + nb1, nrows);
         maxzt = std::max(maxzt, hzoff[e1] - hzoff[b1]);
+        maxpanel = std::max(maxpanel, panel_len[bi]);
     }
-    P->ZT.ensure(std::max<int64_t>(maxzt, 1));
-    P->H.ensure((size_t)nb1 * p * p * NxP);
-    P->G.ensure((size_t)nb3 * P2 * p * p);
-    P->Z.ensure((size_t)P2 * p * nm);
-    MG_CUDA(cudaMemsetAsync(P->Z.p, 0, (size_t)P2 * p * nm * sizeof(double), st));
+    if (dt1) P->ZT.ensure(maxzt);
+    P->panel.ensure(maxpanel);
+    P->H.ensure((size_t)nb1 * pp * NxP);
+    P->G.ensure((size_t)nb3 * pp * P2);
+    P->R.ensure((size_t)nb3 * ldr);
+    P->Sq.ensure((size_t)nb3 * ldq);
+    // K-split of the pair contraction so that its grid fills the 148 SMs
+    const int tiles3 = ceil_div(ncols, Cfg128::BN) * ceil_div(P2, Cfg128::BM);
+    int nsplit = 1;
+    {
+        double best = 0;
+        for (int s = 1; s <= 8; ++s) {
+            int ctas = tiles3 * s;
+            double eff = (double)ctas / (ceil_div(ctas, 148) * 148.0);
+            if (s > 1 && nb3 / s < 4 * PAIR_BK) break;
+            if (eff > best + 0.02) { best = eff; nsplit = s; }
+        }
+    }
+    const int64_t zsplit = (int64_t)P2 * ncols;
+    P->Z.ensure((size_t)nsplit * zsplit);
+    MG_CUDA(cudaMemsetAsync(P->Z.p, 0, (size_t)nsplit * zsplit * sizeof(double), st));
     P->gamma.ensure((size_t)nm * nm);
 
     static bool attr_done = false;
+    const size_t smem_run = RunPipe::smem_bytes;
+    const size_t smem_x = XPipe::smem_bytes;
+    const size_t smem_pair = PairPipe::smem_bytes;
     if (!attr_done) {
         MG_CUDA(cudaFuncSetAttribute(k_run_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)GB_SMEM));
+                                     (int)smem_run));
         MG_CUDA(cudaFuncSetAttribute(k_x_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)GB_SMEM));
+                                     (int)smem_x));
         MG_CUDA(cudaFuncSetAttribute(k_pair_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)GB_SMEM));
+                                     (int)smem_pair));
         attr_done = true;
     }
     DBuf<int> l0d;
@@ -571,7 +628,6 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     double f_run = 0, f_x = 0, f_pair = 0;
     int64_t launches = 0;
     const int cb0 = class_base(P, 0), cb1 = class_base(P, 1);
-    const int l0e = P->l0[0], l0o = P->l0[1];
     const int64_t ldb = (int64_t)p * NxP;
     int bidx = 0;
     for (int64_t b3 = 0; b3 < nrows; b3 += nb3) {
@@ -580,12 +636,8 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             int64_t e1 = std::min<int64_t>(b1 + nb1, e3);
             int nb = (int)(e1 - b1);
             const int64_t zbase = hzoff[b1];
-            prof_mark(P, 0, st);
-            if (!dt1) {
-                k_row_weights<<<nb, 128, 0, st>>>(P->rows.p + b1, P->zoff.p + b1, zbase, P->l_min,
-                                                  l0d.p, P->C.p, P->v.p, P->lf.p, P->h2_mode,
-                                                  P->ZT.p);
-            } else {
+            const double* zt = nullptr;
+            if (dt1) {
                 int64_t t0 = (*tri_of_row)[b1], t1 = (*tri_of_row)[e1];
                 MG_CUDA(cudaMemsetAsync(P->ZT.p, 0, (hzoff[e1] - zbase) * sizeof(double), st));
                 if (t1 > t0)
@@ -593,39 +645,53 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                                         st>>>(dt1 + t0, dt2 + t0, dt3 + t0, dpos + t0, ddup + t0,
                                               t1 - t0, zbase, P->l_min, P->C.p, P->v.p,
                                               P->lf.p, P->h2_mode, P->ZT.p);
+                MG_LAUNCHED();
+                zt = P->ZT.p;
             }
-            MG_LAUNCHED();
             int tf = tile_first[bidx], tl = tile_first[bidx + 1];
-            dim3 g1(ceil_div(ldb, GB_N), tl - tf);
+            prof_mark(P, 0, st);
+            k_run_panels<<<tl - tf, PANEL_THREADS, 0, st>>>(P->tiles.p + tf, P->rows.p, P->poff.p + tf,
+                                                   P->zoff.p, zbase, zt, l0d.p, P->q.p, P->L,
+                                                   P->l_min, p, P->P8, P->C.p, P->v.p, P->lf.p,
+                                                   P->h2_mode, P->panel.p);
+            MG_LAUNCHED();
+            dim3 g1(ceil_div(ldb, Cfg128::BN), tl - tf);
             prof_mark(P, 1, st);
-            k_run_contract<<<g1, GB_THREADS, GB_SMEM, st>>>(
-                P->tiles.p + tf, P->rows.p, P->zoff.p, zbase, (int)b1, P->ZT.p, P->q.p,
-                P->WQT.p, p, P->P8, NxP, P->L, P->l_min, l0e, l0o, cb0, cb1, P->H.p);
+            k_run_contract<<<g1, 256, smem_run, st>>>(P->tiles.p + tf, P->poff.p + tf,
+                                                             P->panel.p, (int)b1, P->rows.p,
+                                                             P->WQT.p, p, P->P8, NxP, cb0, cb1,
+                                                             P->H.p);
             MG_LAUNCHED();
-            dim3 g2(ceil_div(p * p, GB_N), ceil_div(P2, GB_M), nb);
+            dim3 g2(ceil_div(pp, CfgX::BN), ceil_div(P2, CfgX::BM), nb);
             prof_mark(P, 2, st);
-            k_x_contract<<<g2, GB_THREADS, GB_SMEM, st>>>(P->rows.p, (int)b1, (int)b3, P->QT.p,
-                                                          P->H.p, p, P2, NxP, P->l_min, P->G.p);
+            k_x_contract<<<g2, CfgX::THREADS, smem_x, st>>>(P->rows.p, (int)b1, (int)b3, P->QT.p,
+                                                         P->H.p, p, P2, NxP, P->l_min, P->G.p);
             MG_LAUNCHED();
-            launches += 3;
+            launches += 3 + (dt1 ? 1 : 0);
             for (int64_t r = b1; r < e1; ++r) {
                 double m = (double)(hrows[r].jhi - hrows[r].jlo + 1);
                 f_run += 2.0 * p * p * P->Nx * m;
             }
-            f_x += 2.0 * P2 * p * p * P->Nx * nb;
+            f_x += 2.0 * P2 * pp * P->Nx * (double)nb;
         }
-        dim3 g3(ceil_div((int64_t)p * nm, GB_N), ceil_div(P2, GB_M));
+        const int n3 = (int)(e3 - b3);
         prof_mark(P, 3, st);
-        k_pair_contract<<<g3, GB_THREADS, GB_SMEM, st>>>(P->rows.p + b3, (int)(e3 - b3), P->q.p,
-                                                         P->G.p, P->modes.p, p, P2, nm, P->L,
-                                                         P->l_min, P->Z.p);
+        dim3 gg(std::min(ceil_div(ncols, 256), 64), n3);
+        k_gather<<<gg, 256, 0, st>>>(P->rows.p + b3, P->G.p, P->modes.p, P->q.p, P->L, P->l_min,
+                                     p, P2, nm, ldr, ldq, P->R.p, P->Sq.p);
         MG_LAUNCHED();
-        launches += 1;
-        f_pair += 2.0 * P2 * p * nm * (double)(e3 - b3);
+        const int per = (int)round_up(ceil_div(n3, nsplit), PAIR_BK);
+        dim3 g3(ceil_div(ncols, Cfg128::BN), ceil_div(P2, Cfg128::BM), ceil_div(n3, per));
+        prof_mark(P, 4, st);
+        k_pair_contract<<<g3, 256, smem_pair, st>>>(P->Sq.p, ldq, P->R.p, ldr, n3, per,
+                                                           P2, ncols, zsplit, P->Z.p);
+        MG_LAUNCHED();
+        launches += 2;
+        f_pair += 2.0 * P2 * ncols * (double)n3;
     }
-    prof_mark(P, 4, st);
+    prof_mark(P, 5, st);
     k_final<<<std::min<int64_t>(((int64_t)nm * nm + 255) / 256, 4096), 256, 0, st>>>(
-        P->Z.p, P->modes.p, p, nm, P->gamma.p);
+        P->Z.p, nsplit, zsplit, P->modes.p, p, nm, P->gamma.p);
     MG_LAUNCHED();
     prof_mark(P, -1, st);
     launches += 1;
@@ -633,8 +699,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     P->flops_x = f_x;
     P->flops_pair = f_pair;
     P->launches = launches;
-    // keep l0d alive until the stream drains
-    MG_CUDA(cudaStreamSynchronize(st));
+    MG_CUDA(cudaStreamSynchronize(st));  // keeps l0d alive until the stream drains
     prof_collect(P);
 }
 

@@ -19,6 +19,8 @@ struct MgTile {
     int row0, nrows, jlo, jhi;
 };
 
+constexpr int MG_NPROF = 6;
+
 struct mg_plan {
     int device = 0;
     int p = 0, Nx = 0, NxP = 0, nm = 0, l_min = 2, l_max = 2, L = 0, h2_mode = 0;
@@ -30,7 +32,8 @@ struct mg_plan {
     mg::DBuf<double> q, QT, WQT, C, v, lf, wr2;
     mg::DBuf<int> modes;  // [nm][3]
     // scratch
-    mg::DBuf<double> ZT, H, G, Z, gamma;
+    mg::DBuf<double> ZT, panel, H, G, R, Sq, Z, gamma;
+    mg::DBuf<int64_t> poff;
     mg::DBuf<MgRow> rows;
     mg::DBuf<int64_t> zoff;
     mg::DBuf<MgTile> tiles;
@@ -38,9 +41,9 @@ struct mg_plan {
     // stats of the last execute
     double flops_run = 0, flops_x = 0, flops_pair = 0;
     int64_t launches = 0;
-    // optional kernel timing: ms per family {weights, run, x, pair, final}, accumulated
+    // optional kernel timing: ms per family {panels, run, x, gather, pair, final}
     bool profile = false;
-    double prof_ms[5] = {0, 0, 0, 0, 0};
+    double prof_ms[MG_NPROF] = {0, 0, 0, 0, 0, 0};
     std::vector<cudaEvent_t> prof_events;
     std::vector<int> prof_tags;
     size_t prof_used = 0;

@@ -183,16 +183,16 @@ class TestGammaC0:
         assert frob_rel(total, g_c0["gamma"]) < 1e-12
 
 
+@pytest.fixture(scope="module")
+def c1():
+    from paper_1503_08809_b200 import build_qtilde
+    hi = host_inputs("c1")
+    C, qt = build_qtilde(hi)
+    return hi, C, qt
+
+
 class TestGammaLarge:
     """Config-1 scale: flat-range partials vs the oracle on the same (GPU-built) q̃."""
-
-    @pytest.fixture(scope="class")
-    @staticmethod
-    def c1():
-        from paper_1503_08809_b200 import build_qtilde
-        hi = host_inputs("c1")
-        C, qt = build_qtilde(hi)
-        return hi, C, qt
 
     @pytest.mark.parametrize("frac", [0.1, 0.5, 0.9])
     def test_partial_vs_oracle(self, c1, frac):
