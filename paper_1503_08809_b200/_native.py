@@ -16,7 +16,7 @@ import numpy as np
 __all__ = ["lib", "check", "LIB_PATH", "ptr", "MG_H2", "NativeError"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_native", "libmodal_b200.so")
+LIB_PATH = os.environ.get("MG_LIB_PATH") or os.path.join(HERE, "_native", "libmodal_b200.so")
 MG_H2 = {"gosper": 0, "exact": 1}
 
 _i = ctypes.c_int

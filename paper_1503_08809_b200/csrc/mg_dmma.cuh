@@ -104,6 +104,7 @@ enum class ASrc { KMajor, MMajor, Raw };
 
 // Producer contract:
 //   __device__ void issue(int kt, double* As, double* Bs, double* raw) const;   // cp.async
+//   __device__ int kvalid_last() const;   // k values with data in the last k-tile (1..BK)
 //   (ASrc::Raw only) __device__ double a_frag(const double* raw, int k, int fm) const;
 //     — value of A at (m = this lane's row of fragment fm, k) built from staged raw data.
 // Stage layout: [A tile (absent for Raw)][B tile][raw (kRaw doubles)].
@@ -163,15 +164,20 @@ struct Pipe {
                 for (int ni = 0; ni < FN; ++ni)
                     b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g);
             };
+            // k4 steps that hold data (the tail of the last tile is all zeros: skip it)
+            const int nks = kt + 1 < ktiles ? BK / 4 : (prod.kvalid_last() + 3) / 4;
             load_frags(0, t);
 #pragma unroll
             for (int ks = 0; ks < BK / 4; ++ks) {
-                const int cur = ks & 1;
-                if (ks + 1 < BK / 4) load_frags(cur ^ 1, (ks + 1) * 4 + t);
+                if (ks < nks) {
+                    const int cur = ks & 1;
+                    if (ks + 1 < BK / 4) load_frags(cur ^ 1, (ks + 1) * 4 + t);
 #pragma unroll
-                for (int mi = 0; mi < FM; ++mi)
+                    for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-                    for (int ni = 0; ni < FN; ++ni) dmma884(acc.c[mi][ni], a[cur][mi], b[cur][ni]);
+                        for (int ni = 0; ni < FN; ++ni)
+                            dmma884(acc.c[mi][ni], a[cur][mi], b[cur][ni]);
+                }
             }
         }
         cp_async_wait<0>();

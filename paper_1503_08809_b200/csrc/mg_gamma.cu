@@ -34,8 +34,8 @@ namespace mg {
 
 // QT[l][c][x] = q̃[c][x][l] ; WQT[cls(l)][c][x] = wr2[x] q̃[c][x][l]  (x zero-padded to NxP)
 __global__ void k_transpose_qt(const double* __restrict__ qt, const double* __restrict__ wr2,
-                               int p, int Nx, int NxP, int L, int l_min, int l0_1, int n0,
-                               double* __restrict__ QT, double* __restrict__ WQT) {
+                               int p, int Nx, int NxP, int Nxw, int L, int l_min, int l0_1,
+                               int n0, double* __restrict__ QT, double* __restrict__ WQT) {
     int64_t total = (int64_t)L * p * NxP;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -47,7 +47,7 @@ __global__ void k_transpose_qt(const double* __restrict__ qt, const double* __re
         QT[i] = val;
         int l = l_min + li;
         int s = ((l ^ l_min) & 1) == 0 ? (l - l_min) / 2 : n0 + (l - l0_1) / 2;
-        WQT[((int64_t)s * p + c) * NxP + x] = x < Nx ? wr2[x] * val : 0.0;
+        if (x < Nxw) WQT[((int64_t)s * p + c) * Nxw + x] = x < Nx ? wr2[x] * val : 0.0;
     }
 }
 
@@ -73,29 +73,38 @@ constexpr int RUN_BK = 32, RUN_ST = 3;
 constexpr int X_BK = 32, X_ST = 2;
 constexpr int PAIR_BK = 32, PAIR_ST = 3;
 using Cfg128 = TileCfg<2, 4, 8, 4>;  // 128 x 128, 8 warps, 64 accumulators per lane
+#ifndef MG_RUN_WIDE
+#define MG_RUN_WIDE 1
+#endif
+#if MG_RUN_WIDE
+using CfgRun = TileCfg<4, 4, 4, 4>;  // 128 x 128, 16 warps, 32 accumulators per lane
+#else
+using CfgRun = Cfg128;
+#endif
 using CfgX = TileCfg<4, 2, 4, 5>;    // 128 x 80, 8 warps, 40 accumulators per lane
-using RunPipe = Pipe<Cfg128, RUN_BK, RUN_ST, ASrc::KMajor, true, 0>;
+using RunPipe = Pipe<CfgRun, RUN_BK, RUN_ST, ASrc::KMajor, true, 0>;
 using PairPipe = Pipe<Cfg128, PAIR_BK, PAIR_ST, ASrc::KMajor, true, 0>;
 constexpr int GB_M = 128;
 
 constexpr int PANEL_THREADS = 256;
-constexpr int PANEL_JC = 64;  // j values per shared-memory weight chunk
+constexpr int PANEL_JC = 32;  // j values per shared-memory weight chunk
 
+// Slot s (0 <= s < 128) of tile tl is (row, c) = (row0 + (c0 + s) / p, (c0 + s) % p).
 __global__ void __launch_bounds__(PANEL_THREADS)
 k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
              const int64_t* __restrict__ poff, const int64_t* __restrict__ zoff, int64_t zbase,
              const double* __restrict__ ZT, const int* __restrict__ l0,
-             const double* __restrict__ q, int L, int l_min, int p, int P8,
+             const double* __restrict__ q, int L, int l_min, int p,
              const double* __restrict__ C, const double* __restrict__ v,
              const double* __restrict__ lf, int mode, double* __restrict__ panel) {
-    __shared__ double zs[GB_M / 8][PANEL_JC];  // zm of (row, j) for the current j chunk
+    extern __shared__ double zs[];  // [nrows][PANEL_JC]: zm of (row, j) for the current chunk
     const MgTile tl = tiles[blockIdx.x];
     const int kt = (tl.jhi - tl.jlo + RUN_BK) / RUN_BK * RUN_BK;
     double* out = panel + poff[blockIdx.x];
-    const int nrz = tl.nrows;  // <= 16 rows per tile
+    const int par = rows[tl.row0].par;
     for (int jc = 0; jc < kt; jc += PANEL_JC) {
         // 1) each (row, j) weight once
-        for (int e = threadIdx.x; e < nrz * PANEL_JC; e += PANEL_THREADS) {
+        for (int e = threadIdx.x; e < tl.nrows * PANEL_JC; e += PANEL_THREADS) {
             const int rr = e / PANEL_JC, jl = e % PANEL_JC;
             const int j = tl.jlo + jc + jl;
             const MgRow rw = rows[tl.row0 + rr];
@@ -107,20 +116,21 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
                     z = zm_weight(mode, l0[rw.par] + 2 * j, rw.l2, rw.l3, C, v, l_min, lf);
                 }
             }
-            zs[rr][jl] = z;
+            zs[rr * PANEL_JC + jl] = z;
         }
         __syncthreads();
         // 2) panel[j][slot] = zm(row(slot), j) * q_c(slot)(l1(j)), slot-contiguous stores
-        const int par = rows[tl.row0].par;
         for (int e = threadIdx.x; e < PANEL_JC * GB_M; e += PANEL_THREADS) {
             const int jl = e / GB_M, slot = e % GB_M;
             if (jc + jl >= kt) break;
-            const int rr = slot / P8, c = slot - rr * P8;
             double val = 0.0;
-            if (rr < nrz && c < p) {
-                const int l1 = l0[par] + 2 * (tl.jlo + jc + jl);
-                const double z = zs[rr][jl];
-                if (z != 0.0) val = z * q[(int64_t)c * L + (l1 - l_min)];
+            if (slot < tl.nslots) {
+                const int rr = (tl.c0 + slot) / p, c = (tl.c0 + slot) % p;
+                const double z = zs[rr * PANEL_JC + jl];
+                if (z != 0.0) {
+                    const int l1 = l0[par] + 2 * (tl.jlo + jc + jl);
+                    val = z * q[(int64_t)c * L + (l1 - l_min)];
+                }
             }
             out[(int64_t)(jc + jl) * GB_M + slot] = val;
         }
@@ -129,48 +139,59 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
 }
 
 // ------------------------------------------------------------------------------------------
-// K1: run contraction  H[(r,c)][(c',x)] = Σ_j panel[j][(r,c)] WQT[cls+j][(c',x)]
+// K1: run contraction  H[slot][(c',x)] = Σ_j panel[j][slot] WQT[cls+j][(c',x)]
+//   slot = (row, c) flattened over the batch; WQT rows are p*Nxw wide (x unpadded when Nx is
+//   even); H rows are [c'][NxP] (x padded to the x-contraction's BK, pads stay zero).
 // ------------------------------------------------------------------------------------------
 struct RunProd {
     const double* panel;  // this tile's panel
     const double* wqt;    // WQT + cls*ldb + n0
     int64_t ldb;
-    int jlo, jhi, n_valid;
+    int jlo, jhi, n_valid, kv_last;
+    __device__ int kvalid_last() const { return kv_last; }
     __device__ void issue(int kt, double* As, double* Bs, double*) const {
-        copy_kmajor<RUN_BK, 128, 256>(
+        copy_kmajor<RUN_BK, 128, CfgRun::THREADS>(
             As, [&](int k) { return panel + (int64_t)(kt * RUN_BK + k) * GB_M; }, GB_M);
-        copy_kmajor<RUN_BK, 128, 256>(Bs, [&](int k) -> const double* {
+        copy_kmajor<RUN_BK, 128, CfgRun::THREADS>(Bs, [&](int k) -> const double* {
             int j = jlo + kt * RUN_BK + k;
             return j <= jhi ? wqt + (int64_t)j * ldb : nullptr;
         }, n_valid);
     }
 };
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(CfgRun::THREADS, 1)
 k_run_contract(const MgTile* __restrict__ tiles, const int64_t* __restrict__ poff,
                const double* __restrict__ panel, int row_base, const MgRow* __restrict__ rows,
-               const double* __restrict__ WQT, int p, int P8, int NxP, int cbase0, int cbase1,
-               double* __restrict__ H) {
+               const double* __restrict__ WQT, int p, int Nx, int Nxw, int NxP, int cbase0,
+               int cbase1, double* __restrict__ H) {
     extern __shared__ __align__(16) double smem[];
     const MgTile tl = tiles[blockIdx.y];
-    const int n0 = blockIdx.x * Cfg128::BN;
-    const int64_t ldb = (int64_t)p * NxP;
+    const int n0 = blockIdx.x * CfgRun::BN;
+    const int64_t ldb = (int64_t)p * Nxw;
     const int par = rows[tl.row0].par;
+    const int nk = tl.jhi - tl.jlo + 1;
     RunProd pr;
     pr.panel = panel + poff[blockIdx.y];
     pr.wqt = WQT + (int64_t)(par ? cbase1 : cbase0) * ldb + n0;
     pr.ldb = ldb;
     pr.jlo = tl.jlo;
     pr.jhi = tl.jhi;
-    pr.n_valid = (int)(ldb - n0 < Cfg128::BN ? ldb - n0 : Cfg128::BN);
-    Acc<Cfg128> acc;
-    RunPipe::run((tl.jhi - tl.jlo + RUN_BK) / RUN_BK, pr, smem, acc);
-    acc_foreach_pair<Cfg128>(acc, [&](int m, int n, double v0, double v1) {
-        int rr = m / P8, c = m - rr * P8;
-        int gn = n0 + n;
-        if (rr < tl.nrows && c < p && gn < ldb) {
-            int64_t hr = (int64_t)(tl.row0 + rr - row_base) * p + c;
-            *reinterpret_cast<double2*>(H + hr * ldb + gn) = make_double2(v0, v1);
+    pr.n_valid = (int)(ldb - n0 < CfgRun::BN ? ldb - n0 : CfgRun::BN);
+    pr.kv_last = nk - (nk - 1) / RUN_BK * RUN_BK;
+    Acc<CfgRun> acc;
+    RunPipe::run((nk + RUN_BK - 1) / RUN_BK, pr, smem, acc);
+    const int64_t hbase = (int64_t)(tl.row0 - row_base) * p + tl.c0;  // H row of slot 0
+    const int64_t ldh = (int64_t)p * NxP;
+    acc_foreach_pair<CfgRun>(acc, [&](int m, int n, double v0, double v1) {
+        const int gn = n0 + n;
+        if (m < tl.nslots && gn < ldb) {
+            const int cp = gn / Nxw, x = gn - cp * Nxw;   // Nxw even: (gn, gn+1) share c'
+            double* h = H + (hbase + m) * ldh + (int64_t)cp * NxP + x;
+            if (x + 1 < Nx) {
+                *reinterpret_cast<double2*>(h) = make_double2(v0, v1);
+            } else if (x < Nx) {
+                h[0] = v0;
+            }
         }
     });
 }
@@ -204,6 +225,8 @@ struct XProd {
     const double* h;   // H row (pp x NxP)
     int p, NxP, pp, n0;
     int off[CfgX::FM];  // per fragment: a*X_LDR | (b*X_LDR) << 16 of this lane's pair
+    int kv_last;
+    __device__ int kvalid_last() const { return kv_last; }
     __device__ void issue(int kt, double*, double* Bs, double* raw) const {
         const int cpr = X_BK / 2;  // chunks per q̃ row slice
         for (int c = threadIdx.x; c < 2 * p * cpr; c += CfgX::THREADS) {
@@ -232,7 +255,7 @@ struct XProd {
 __global__ void __launch_bounds__(CfgX::THREADS, MG_X_MINB)
 k_x_contract(const MgRow* __restrict__ rows, int row_b1, int row_b3,
              const double* __restrict__ QT, const double* __restrict__ H, int p, int P2,
-             int NxP, int l_min, double* __restrict__ G) {
+             int Nx, int NxP, int l_min, double* __restrict__ G) {
     extern __shared__ __align__(16) double smem[];
     const int r = blockIdx.z;  // row within the K1/K2 batch
     const MgRow rw = rows[row_b1 + r];
@@ -246,6 +269,7 @@ k_x_contract(const MgRow* __restrict__ rows, int row_b1, int row_b3,
     pr.NxP = NxP;
     pr.pp = pp;
     pr.n0 = n0;
+    pr.kv_last = Nx - (NxP / X_BK - 1) * X_BK;
 #pragma unroll
     for (int fm = 0; fm < CfgX::FM; ++fm) {
         int prr = m0 + frag_row<CfgX>(fm);
@@ -320,6 +344,7 @@ struct PairProd {
     int ldq;
     int64_t ldr;
     int nr, m_valid, n_valid;
+    __device__ int kvalid_last() const { return nr - (nr - 1) / PAIR_BK * PAIR_BK; }
     __device__ void issue(int kt, double* As, double* Bs, double*) const {
         copy_kmajor<PAIR_BK, 128, 256>(As, [&](int k) -> const double* {
             int r = kt * PAIR_BK + k;
@@ -416,8 +441,7 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
     P->h2_mode = h2_mode;
     P->NxP = (int)round_up(Nx, X_BK);
     P->P2 = p * (p + 1) / 2;
-    P->P8 = (int)round_up(p, 8);
-    P->rpt = std::max(1, GB_M / P->P8);
+    P->Nxw = (Nx % 2 == 0) ? Nx : P->NxP;
     P->l0[l_min & 1] = l_min;
     P->l0[(l_min + 1) & 1] = l_min + 1;
     P->nclass[l_min & 1] = (L + 1) / 2;
@@ -441,12 +465,12 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
         qt_src = staged.p;
     }
     P->QT.alloc((size_t)L * p * P->NxP);
-    P->WQT.alloc((size_t)L * p * P->NxP);
+    P->WQT.alloc((size_t)L * p * P->Nxw);
     // classes: even-parity l first when l_min is even (class of l_min is class 0 in storage)
     // storage index s(l) = (l - l_min)/2 for the parity of l_min, n0 + (l - l0')/2 otherwise
     int n0 = (L + 1) / 2;
-    k_transpose_qt<<<1184, 256>>>(qt_src, P->wr2.p, p, Nx, P->NxP, L, l_min, l_min + 1, n0,
-                                  P->QT.p, P->WQT.p);
+    k_transpose_qt<<<1184, 256>>>(qt_src, P->wr2.p, p, Nx, P->NxP, P->Nxw, L, l_min,
+                                  l_min + 1, n0, P->QT.p, P->WQT.p);
     MG_LAUNCHED();
     MG_CUDA(cudaDeviceSynchronize());
 }
@@ -544,33 +568,43 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     const int64_t ldr = round_up(ncols, 2);
     const int ldq = (int)round_up(P2, 2);
 
-    // tiles: consecutive rows of one (l2, par) group, at most rpt per tile, per nb1-batch;
-    // each tile owns a k-major A panel of round_up(window, RUN_BK) x 128 doubles.
+    // tiles: 128 consecutive (row, c) slots of one (l2, par) group (rows may straddle two
+    // tiles), per nb1-batch; each tile owns a k-major A panel of round_up(window, BK) x 128.
     std::vector<MgTile> tiles;
     std::vector<int64_t> poff;      // panel offset of each tile, relative to its batch
     std::vector<int> tile_first;    // per nb1 batch
     std::vector<int64_t> panel_len; // per nb1 batch
+    int max_tile_rows = 1;
     for (int64_t b1 = 0; b1 < nrows; b1 += nb1) {
         int64_t e1 = std::min<int64_t>(b1 + nb1, nrows);
         tile_first.push_back((int)tiles.size());
         int64_t off = 0;
-        int64_t i = b1;
-        while (i < e1) {
-            MgTile t;
-            t.row0 = (int)i;
-            t.nrows = 0;
-            t.jlo = hrows[i].jlo;
-            t.jhi = hrows[i].jhi;
-            while (i < e1 && t.nrows < P->rpt && hrows[i].l2 == hrows[t.row0].l2 &&
-                   hrows[i].par == hrows[t.row0].par) {
-                t.jlo = std::min(t.jlo, hrows[i].jlo);
-                t.jhi = std::max(t.jhi, hrows[i].jhi);
-                ++t.nrows;
-                ++i;
+        int64_t g0 = b1;
+        while (g0 < e1) {  // one (l2, par) group [g0, g1)
+            int64_t g1 = g0;
+            while (g1 < e1 && hrows[g1].l2 == hrows[g0].l2 && hrows[g1].par == hrows[g0].par) ++g1;
+            const int64_t nsl = (g1 - g0) * p;
+            for (int64_t s0 = 0; s0 < nsl; s0 += GB_M) {
+                MgTile t;
+                const int64_t s1 = std::min<int64_t>(s0 + GB_M, nsl);
+                t.row0 = (int)(g0 + s0 / p);
+                t.c0 = (int)(s0 % p);
+                t.nslots = (int)(s1 - s0);
+                const int rlast = (int)(g0 + (s1 - 1) / p);
+                t.nrows = rlast - t.row0 + 1;
+                t.jlo = hrows[t.row0].jlo;
+                t.jhi = hrows[t.row0].jhi;
+                for (int r = t.row0; r <= rlast; ++r) {
+                    t.jlo = std::min(t.jlo, hrows[r].jlo);
+                    t.jhi = std::max(t.jhi, hrows[r].jhi);
+                }
+                t.pad0 = t.pad1 = 0;
+                max_tile_rows = std::max(max_tile_rows, t.nrows);
+                tiles.push_back(t);
+                poff.push_back(off);
+                off += round_up(t.jhi - t.jlo + 1, RUN_BK) * GB_M;
             }
-            tiles.push_back(t);
-            poff.push_back(off);
-            off += round_up(t.jhi - t.jlo + 1, RUN_BK) * GB_M;
+            g0 = g1;
         }
         panel_len.push_back(off);
     }
@@ -588,7 +622,10 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     }
     if (dt1) P->ZT.ensure(maxzt);
     P->panel.ensure(maxpanel);
-    P->H.ensure((size_t)nb1 * pp * NxP);
+    if (P->H.n < (size_t)nb1 * pp * NxP) {  // x pads of H are never written: zero them once
+        P->H.ensure((size_t)nb1 * pp * NxP);
+        MG_CUDA(cudaMemsetAsync(P->H.p, 0, P->H.n * sizeof(double), st));
+    }
     P->G.ensure((size_t)nb3 * pp * P2);
     P->R.ensure((size_t)nb3 * ldr);
     P->Sq.ensure((size_t)nb3 * ldq);
@@ -628,7 +665,6 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     double f_run = 0, f_x = 0, f_pair = 0;
     int64_t launches = 0;
     const int cb0 = class_base(P, 0), cb1 = class_base(P, 1);
-    const int64_t ldb = (int64_t)p * NxP;
     int bidx = 0;
     for (int64_t b3 = 0; b3 < nrows; b3 += nb3) {
         int64_t e3 = std::min<int64_t>(b3 + nb3, nrows);
@@ -650,22 +686,23 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             }
             int tf = tile_first[bidx], tl = tile_first[bidx + 1];
             prof_mark(P, 0, st);
-            k_run_panels<<<tl - tf, PANEL_THREADS, 0, st>>>(P->tiles.p + tf, P->rows.p, P->poff.p + tf,
-                                                   P->zoff.p, zbase, zt, l0d.p, P->q.p, P->L,
-                                                   P->l_min, p, P->P8, P->C.p, P->v.p, P->lf.p,
-                                                   P->h2_mode, P->panel.p);
+            k_run_panels<<<tl - tf, PANEL_THREADS, max_tile_rows * PANEL_JC * sizeof(double),
+                           st>>>(P->tiles.p + tf, P->rows.p, P->poff.p + tf, P->zoff.p, zbase, zt,
+                                 l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p,
+                                 P->h2_mode, P->panel.p);
             MG_LAUNCHED();
-            dim3 g1(ceil_div(ldb, Cfg128::BN), tl - tf);
+            dim3 g1(ceil_div((int64_t)p * P->Nxw, CfgRun::BN), tl - tf);
             prof_mark(P, 1, st);
-            k_run_contract<<<g1, 256, smem_run, st>>>(P->tiles.p + tf, P->poff.p + tf,
+            k_run_contract<<<g1, CfgRun::THREADS, smem_run, st>>>(P->tiles.p + tf, P->poff.p + tf,
                                                              P->panel.p, (int)b1, P->rows.p,
-                                                             P->WQT.p, p, P->P8, NxP, cb0, cb1,
-                                                             P->H.p);
+                                                             P->WQT.p, p, P->Nx, P->Nxw, NxP, cb0,
+                                                             cb1, P->H.p);
             MG_LAUNCHED();
             dim3 g2(ceil_div(pp, CfgX::BN), ceil_div(P2, CfgX::BM), nb);
             prof_mark(P, 2, st);
             k_x_contract<<<g2, CfgX::THREADS, smem_x, st>>>(P->rows.p, (int)b1, (int)b3, P->QT.p,
-                                                         P->H.p, p, P2, NxP, P->l_min, P->G.p);
+                                                         P->H.p, p, P2, P->Nx, NxP, P->l_min,
+                                                         P->G.p);
             MG_LAUNCHED();
             launches += 3 + (dt1 ? 1 : 0);
             for (int64_t r = b1; r < e1; ++r) {

@@ -14,9 +14,10 @@
 struct MgRow {
     int l2, l3, par, jlo, jhi, pad;
 };
-// One M-tile of the run-contraction GEMM: up to `rpt` consecutive rows of one parity class.
+// One M-tile of the run-contraction GEMM: `nslots` (<= 128) consecutive (row, c) slots of one
+// (l2, parity) group, starting at slot c0 of row row0 (global row index); rows touched: nrows.
 struct MgTile {
-    int row0, nrows, jlo, jhi;
+    int row0, c0, nslots, nrows, jlo, jhi, pad0, pad1;
 };
 
 constexpr int MG_NPROF = 6;
@@ -25,8 +26,7 @@ struct mg_plan {
     int device = 0;
     int p = 0, Nx = 0, NxP = 0, nm = 0, l_min = 2, l_max = 2, L = 0, h2_mode = 0;
     int P2 = 0;        // p(p+1)/2 unordered basis pairs
-    int P8 = 0;        // p rounded up to 8 (slot stride of the run-contraction tile)
-    int rpt = 0;       // rows per run-contraction tile = 128 / P8
+    int Nxw = 0;       // x stride of WQT rows (Nx when even, else NxP)
     int l0[2] = {0, 0};      // first l of each parity class
     int nclass[2] = {0, 0};  // number of l in each parity class
     mg::DBuf<double> q, QT, WQT, C, v, lf, wr2;

@@ -1,7 +1,17 @@
 import os
 import sys
 
-import numpy as np
+# one BLAS thread per process: the oracle forks worker pools (like the reference's
+# multiprocessing sweep), and forking after OpenBLAS has started threads can deadlock
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+from threadpoolctl import threadpool_limits  # noqa: E402
+
+# numpy may already be imported (pytest plugins) with a multi-threaded BLAS: pin it to one
+# thread so the fork pools of the oracle neither deadlock nor oversubscribe
+threadpool_limits(1)
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

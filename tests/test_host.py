@@ -1,0 +1,161 @@
+"""CPU: host logic of the drop-in (mirror types, plans, shard balance, configs) and the
+C-ABI library (loads, exports every symbol of include/modal_b200.h, fails loudly without a
+GPU).  No compute call needs a device here."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1503_08809_b200 as mg
+from conftest import ROOT
+from paper_1503_08809_b200 import _native
+from paper_1503_08809_b200.configs import CONFIGS, host_inputs, sparse_domain, sparse_grid
+from paper_1503_08809_b200.scheduler import slab_costs
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "modal_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(mg_\w+)\(", text, re.M)))
+
+
+class TestABI:
+    def test_library_exports_every_header_symbol(self):
+        lib = _native.lib()
+        syms = header_symbols()
+        assert len(syms) >= 20
+        for s in syms:
+            assert hasattr(lib, s), s
+            assert s in _native._SIGS, f"{s} missing from the ctypes binding"
+
+    def test_library_is_sm100a(self):
+        import subprocess
+        out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH],
+                             capture_output=True, text=True).stdout
+        assert "sm_100a" in out
+
+    def test_host_only_entry_points(self):
+        lib = _native.lib()
+        assert lib.mg_version() >= 100
+        c, r = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        assert lib.mg_domain_count(2, 2000, _native.ptr(c), _native.ptr(r)) == 0
+        assert c[0] == 334_831_501
+        assert lib.mg_domain_count(1, 4, _native.ptr(c), None) == 1     # ValueError code
+        assert b"l_min" in lib.mg_last_error()
+
+    def test_no_gpu_fails_loudly(self):
+        if _native.lib().mg_device_count() > 0:
+            pytest.skip("a GPU is present")
+        with pytest.raises(RuntimeError, match="no CUDA device"):
+            mg.triple_weights(np.ones(3), np.ones(3), 2, 4)
+
+    def test_slab_plan_matches_python(self):
+        b = np.zeros(9, np.int32)
+        for spec in CONFIGS.values():
+            _native.check(_native.lib().mg_slab_plan(2, spec.l_max, spec.p, spec.n_x, 8,
+                                                     _native.ptr(b)))
+            assert b.tolist() == mg.slab_plan(2, spec.l_max, spec.p, spec.n_x, 8)
+
+
+class TestMirrorTypes:
+    def test_default_mapping(self):
+        m = mg.default_mode_mapping(3)
+        assert m.n_max == 10
+        assert m.triple(0) == (0, 0, 0) and m.triple(9) == (2, 2, 2)
+        assert mg.default_mode_mapping(30).n_max == 4960
+
+    def test_mapping_validation(self):
+        with pytest.raises(ValueError):
+            mg.ModeMapping(np.array([[1, 0, 0]]), 2)
+        with pytest.raises(ValueError):
+            mg.ModeMapping(np.array([[0, 0, 1], [0, 0, 1]]), 2)
+        with pytest.raises(ValueError):
+            mg.ModeMapping(np.zeros((0, 3)), 2)
+
+    def test_tables_validation(self):
+        q = np.ones((2, 3))
+        qt = np.ones((2, 4, 3))
+        with pytest.raises(ValueError):
+            mg.BasisTables(q, qt, np.array([1.0, 0.0, 1.0]), np.ones(3), 2, 4)
+        with pytest.raises(ValueError):
+            mg.BasisTables(q, qt, np.ones(4), np.ones(3), 2, 4)
+        t = mg.BasisTables(q, qt, np.ones(3), np.ones(3), 2, 4)
+        assert t.p_max == 2 and t.n_radial == 4
+
+    def test_fingerprints_match_reference_scheme(self, g_desk):
+        # same sha256 recipe as basis.py:50-54,93-94,189-190,259-262
+        import hashlib
+        e = g_desk["desk_entries"]
+        m = mg.ModeMapping(e, 3)
+        h = hashlib.sha256(np.int64(3).tobytes() + e.astype(np.int64).tobytes()).hexdigest()[:16]
+        assert m.fingerprint() == h
+
+    def test_gamma_container(self):
+        with pytest.raises(ValueError):
+            mg.GammaMatrix(np.array([[np.nan]]))
+        with pytest.raises(ValueError):
+            mg.GammaMatrix(np.zeros(3))
+
+    def test_shifted_legendre_bit_exact(self, g_desk):
+        assert np.array_equal(mg.shifted_legendre(3, 2, 16), g_desk["desk_q"])
+
+
+class TestScheduler:
+    def test_make_plan_golden(self, g_domain):                # test_scheduler.py:10-17
+        assert np.array_equal(np.array(mg.make_plan(12, 4).ranges), g_domain["plan_12_4"])
+        assert np.array_equal(np.array(mg.make_plan(10, 4).ranges), g_domain["plan_10_4"])
+
+    @pytest.mark.parametrize("total,w", [(0, 3), (7, 1), (2, 5), (10**6, 256)])
+    def test_make_plan_cover(self, total, w):
+        r = mg.make_plan(total, w).ranges
+        assert r[0][0] == 0 and r[-1][1] == total
+        sizes = [b - a for a, b in r]
+        assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)
+
+    def test_merge_partials_order(self):
+        meta = {"tables": "t", "grid": "g", "mapping": "m"}
+        parts = [mg.GammaMatrix(np.array([[v]]), dict(meta)) for v in (1.0, 10.0, 100.0)]
+        out = mg.merge_partials(parts)
+        assert out.values[0, 0] == 111.0 and out.meta["workers_merged"] == 3
+        bad = mg.GammaMatrix(np.array([[1.0]]), dict(meta, tables="x"))
+        with pytest.raises(ValueError):
+            mg.merge_partials([parts[0], bad])
+
+    @pytest.mark.parametrize("cfg", ["c1", "c2", "c4"])
+    def test_slab_balance(self, cfg):
+        spec = CONFIGS[cfg]
+        cost = slab_costs(2, spec.l_max, spec.p, spec.n_x)
+        for n in (2, 4, 8):
+            b = mg.slab_plan(2, spec.l_max, spec.p, spec.n_x, n)
+            assert b[0] == 2 and b[-1] == spec.l_max + 1 and b == sorted(b)
+            shares = [cost[b[i] - 2:b[i + 1] - 2].sum() for i in range(n)]
+            assert max(shares) / (sum(shares) / n) < 1.01
+
+
+class TestConfigs:
+    def test_shapes(self):
+        hi = host_inputs("c1")
+        assert hi.eps.shape == (1999, 3000) and hi.q.shape == (15, 1999)
+        assert hi.qk.shape == (15, 3000) and hi.entries.shape == (680, 3)
+
+    def test_alpha_drawn_after_eps(self):
+        hi = host_inputs("c3")
+        rng = np.random.default_rng(3)
+        rng.standard_normal((1999, 2000))
+        e = mg.default_mode_mapping(8).entries
+        assert np.array_equal(hi.alpha, rng.standard_normal(120) / (1.0 + e.sum(1)))
+
+    def test_sparse_grid(self):
+        g, w = sparse_grid()
+        assert g.size == 244 and g[48] == 50 and g[49] == 60 and g[-1] == 2000
+        assert w[0] == 1.0 and w[48] == 5.5 and w[49] == 10.0 and w[-1] == 5.5
+        # step-1 grid: unit weights and exactly the reference domain
+        g1, w1 = sparse_grid(l_max=30, dense_to=30)
+        assert np.all(w1 == 1.0)
+        l1, l2, l3, W = sparse_domain(g1, w1)
+        from oracle import ref
+        want = ref.domain_triples(2, 30)
+        assert np.array_equal(l1, want[0]) and np.array_equal(l2, want[1])
+        assert np.array_equal(l3, want[2]) and np.all(W == 1.0)
