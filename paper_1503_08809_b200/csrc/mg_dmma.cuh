@@ -143,14 +143,17 @@ struct Pipe {
             const double* As = st;
             const double* Bs = st + SA;
             const double* raw = st + SA + SB;
-            {   // refill the stage consumed in iteration kt-1
+            // refill of the stage consumed in iteration kt-1 (safe after the barrier above);
+            // issued after the first k4 step's DMMAs so the address/issue work of cp.async
+            // overlaps tensor work instead of delaying it
+            auto refill = [&]() {
                 int nk = kt + STAGES - 1;
                 if (nk < ktiles) {
                     double* ns = smem + (nk % STAGES) * SS;
                     prod.issue(nk, ns, ns + SA, ns + SA + SB);
                 }
                 cp_async_commit();
-            }
+            };
             double a[2][FM], b[2][FN];
             auto load_frags = [&](int buf, int k) {
 #pragma unroll
@@ -178,6 +181,7 @@ struct Pipe {
                         for (int ni = 0; ni < FN; ++ni)
                             dmma884(acc.c[mi][ni], a[cur][mi], b[cur][ni]);
                 }
+                if (ks == 0) refill();
             }
         }
         cp_async_wait<0>();

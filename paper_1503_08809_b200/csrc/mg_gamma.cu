@@ -70,7 +70,7 @@ __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t*
 //   panel[jl][slot=(r,c)] = zm(l1(j), l2_r, l3_r) q_c(l1(j))  (0 outside row r's window)
 // ------------------------------------------------------------------------------------------
 constexpr int RUN_BK = 32, RUN_ST = 3;
-constexpr int X_BK = 32, X_ST = 2;
+constexpr int X_BK = 32;
 constexpr int PAIR_BK = 32, PAIR_ST = 3;
 using Cfg128 = TileCfg<2, 4, 8, 4>;  // 128 x 128, 8 warps, 64 accumulators per lane
 #ifndef MG_RUN_WIDE
@@ -81,7 +81,6 @@ using CfgRun = TileCfg<4, 4, 4, 4>;  // 128 x 128, 16 warps, 32 accumulators per
 #else
 using CfgRun = Cfg128;
 #endif
-using CfgX = TileCfg<4, 2, 4, 5>;    // 128 x 80, 8 warps, 40 accumulators per lane
 using RunPipe = Pipe<CfgRun, RUN_BK, RUN_ST, ASrc::KMajor, true, 0>;
 using PairPipe = Pipe<Cfg128, PAIR_BK, PAIR_ST, ASrc::KMajor, true, 0>;
 constexpr int GB_M = 128;
@@ -198,8 +197,10 @@ k_run_contract(const MgTile* __restrict__ tiles, const int64_t* __restrict__ pof
 
 // ------------------------------------------------------------------------------------------
 // K2: x contraction  G[r][(c,c')][ab] = Σ_x S_ab(x) H[r][(c,c')][x]
-//   A = S (pairs x x, built in shared memory from the staged q̃(l2), q̃(l3) slices),
-//   B = H row (m-major, streamed by cp.async).
+//   K2a writes the pair products S[r][ab][x] = q̃_a(x,l2)q̃_b(x,l3) + q̃_b(x,l2)q̃_a(x,l3) of the
+//   batch (elementwise, <2 % of K2's time in bytes), so K2 is a pure cp.async GEMM with both
+//   operands m-major (x contiguous).  The CTA tile is chosen per config to minimise padding
+//   of M = p(p+1)/2 and N = p^2 (120x120 for p = 15, 30; 128x128 for p = 22).
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void pair_of(int pr, int& a, int& b) {
     int bb = (int)((sqrt(8.0 * pr + 1.0) - 1.0) * 0.5);
@@ -212,90 +213,86 @@ __device__ __forceinline__ int pair_idx(int a, int b) {  // a <= b
     return b * (b + 1) / 2 + a;
 }
 
-// raw row stride: 16-byte aligned and = 4 (mod 16) doubles, so the fragment-level reads of
-// rows a, a+1, a+2, a+3 (lanes g) at k0+t land in disjoint 8-bank windows
-constexpr int X_LDR = X_BK + 4;
-constexpr int X_ZROW = 32;              // all-zero row (pairs past P2 point here)
-constexpr int X_RAW = 2 * 33 * X_LDR;   // q̃(l2)[c][k] rows 0..32, then q̃(l3)[c][k] rows 0..32
-using XPipe = Pipe<CfgX, X_BK, X_ST, ASrc::Raw, false, X_RAW>;
+constexpr int PP_CHUNK = 8;  // pairs per block of the pair-product kernel
 
-struct XProd {
-    const double* q2;  // QT[l2] (p x NxP)
-    const double* q3;  // QT[l3]
-    const double* h;   // H row (pp x NxP)
-    int p, NxP, pp, n0;
-    int off[CfgX::FM];  // per fragment: a*X_LDR | (b*X_LDR) << 16 of this lane's pair
-    int kv_last;
-    __device__ int kvalid_last() const { return kv_last; }
-    __device__ void issue(int kt, double*, double* Bs, double* raw) const {
-        const int cpr = X_BK / 2;  // chunks per q̃ row slice
-        for (int c = threadIdx.x; c < 2 * p * cpr; c += CfgX::THREADS) {
-            int which = c / (p * cpr), rem = c % (p * cpr);
-            int cc = rem / cpr, k = (rem % cpr) * 2;
-            const double* src = (which ? q3 : q2) + (int64_t)cc * NxP + kt * X_BK + k;
-            cp_async16(raw + (which * 33 + cc) * X_LDR + k, src, 16);
+__global__ void __launch_bounds__(256)
+k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __restrict__ QT,
+                int p, int P2, int NxP, int l_min, double* __restrict__ S) {
+    const int r = blockIdx.y;
+    const MgRow rw = rows[row_b1 + r];
+    const double2* q2 = reinterpret_cast<const double2*>(QT + (int64_t)(rw.l2 - l_min) * p * NxP);
+    const double2* q3 = reinterpret_cast<const double2*>(QT + (int64_t)(rw.l3 - l_min) * p * NxP);
+    double2* out = reinterpret_cast<double2*>(S + (int64_t)r * P2 * NxP);
+    const int nx2 = NxP / 2;
+    int pr = blockIdx.x * PP_CHUNK, a, b;
+    pair_of(pr, a, b);
+    for (int i = 0; i < PP_CHUNK && pr < P2; ++i, ++pr) {
+        const double2* a2 = q2 + a * nx2;
+        const double2* b2 = q2 + b * nx2;
+        const double2* a3 = q3 + a * nx2;
+        const double2* b3 = q3 + b * nx2;
+        for (int x = threadIdx.x; x < nx2; x += blockDim.x) {
+            double2 u = a2[x], w = b3[x], y = b2[x], z = a3[x];
+            out[(int64_t)pr * nx2 + x] = make_double2(u.x * w.x + y.x * z.x, u.y * w.y + y.y * z.y);
         }
-        copy_mmajor<X_BK, CfgX::BN, CfgX::THREADS>(Bs, [&](int m) -> const double* {
-            int cc = n0 + m;
-            return cc < pp ? h + (int64_t)cc * NxP + kt * X_BK : nullptr;
-        }, X_BK);
+        if (++a > b) { ++b; a = 0; }  // next pair in b-major order
     }
-    // S_ab(x_k) = q̃_a(x,l2) q̃_b(x,l3) + q̃_b(x,l2) q̃_a(x,l3)   (branch-free: pads read zeros)
-    __device__ double a_frag(const double* raw, int k, int fm) const {
-        const int o = off[fm];
-        const int oa = o & 0xffff, ob = o >> 16;
-        const double* r3 = raw + 33 * X_LDR;
-        return raw[oa + k] * r3[ob + k] + raw[ob + k] * r3[oa + k];
+}
+
+using CfgX120 = TileCfg<5, 3, 3, 5>;  // 120 x 120, 15 warps, 30 accumulators per lane
+template <class Cfg>
+using XPipeT = Pipe<Cfg, X_BK, 3, ASrc::MMajor, false, 0>;
+
+template <class Cfg>
+struct XProd {
+    const double* s;   // S row block of this CTA: S[r] + m0*NxP
+    const double* h;   // H row block: H[r] + n0*NxP
+    int NxP, m_valid, n_valid, kv_last;
+    __device__ int kvalid_last() const { return kv_last; }
+    __device__ void issue(int kt, double* As, double* Bs, double*) const {
+        copy_mmajor<X_BK, Cfg::BM, Cfg::THREADS>(As, [&](int m) -> const double* {
+            return m < m_valid ? s + (int64_t)m * NxP + kt * X_BK : nullptr;
+        }, X_BK);
+        copy_mmajor<X_BK, Cfg::BN, Cfg::THREADS>(Bs, [&](int m) -> const double* {
+            return m < n_valid ? h + (int64_t)m * NxP + kt * X_BK : nullptr;
+        }, X_BK);
     }
 };
 
-#ifndef MG_X_MINB
-#define MG_X_MINB 2
-#endif
-__global__ void __launch_bounds__(CfgX::THREADS, MG_X_MINB)
-k_x_contract(const MgRow* __restrict__ rows, int row_b1, int row_b3,
-             const double* __restrict__ QT, const double* __restrict__ H, int p, int P2,
-             int Nx, int NxP, int l_min, double* __restrict__ G) {
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+k_x_contract(const double* __restrict__ S, const double* __restrict__ H, int row_b1,
+             int row_b3, int p, int P2, int Nx, int NxP, double* __restrict__ G) {
     extern __shared__ __align__(16) double smem[];
     const int r = blockIdx.z;  // row within the K1/K2 batch
-    const MgRow rw = rows[row_b1 + r];
-    const int m0 = blockIdx.y * CfgX::BM, n0 = blockIdx.x * CfgX::BN;
+    const int m0 = blockIdx.y * Cfg::BM, n0 = blockIdx.x * Cfg::BN;
     const int pp = p * p;
-    XProd pr;
-    pr.q2 = QT + (int64_t)(rw.l2 - l_min) * p * NxP;
-    pr.q3 = QT + (int64_t)(rw.l3 - l_min) * p * NxP;
-    pr.h = H + (int64_t)r * pp * NxP;
-    pr.p = p;
+    XProd<Cfg> pr;
+    pr.s = S + ((int64_t)r * P2 + m0) * NxP;
+    pr.h = H + ((int64_t)r * pp + n0) * NxP;
     pr.NxP = NxP;
-    pr.pp = pp;
-    pr.n0 = n0;
+    pr.m_valid = min(Cfg::BM, P2 - m0);
+    pr.n_valid = min(Cfg::BN, pp - n0);
     pr.kv_last = Nx - (NxP / X_BK - 1) * X_BK;
-#pragma unroll
-    for (int fm = 0; fm < CfgX::FM; ++fm) {
-        int prr = m0 + frag_row<CfgX>(fm);
-        if (prr < P2) {
-            int a, b;
-            pair_of(prr, a, b);
-            pr.off[fm] = a * X_LDR | ((b * X_LDR) << 16);
-        } else {
-            pr.off[fm] = X_ZROW * X_LDR | ((X_ZROW * X_LDR) << 16);
-        }
-    }
-    for (int i = threadIdx.x; i < X_ST * X_LDR; i += CfgX::THREADS) {  // zero rows, all stages
-        double* st = smem + (i / X_LDR) * XPipe::SS + XPipe::SA + XPipe::SB;
-        st[X_ZROW * X_LDR + i % X_LDR] = 0.0;
-        st[(33 + X_ZROW) * X_LDR + i % X_LDR] = 0.0;
-    }
-    Acc<CfgX> acc;
-    XPipe::run(NxP / X_BK, pr, smem, acc);
+    Acc<Cfg> acc;
+    XPipeT<Cfg>::run(NxP / X_BK, pr, smem, acc);
     double* Gr = G + (int64_t)(row_b1 + r - row_b3) * pp * P2;
-    acc_foreach_pair<CfgX>(acc, [&](int m, int n, double v0, double v1) {
+    acc_foreach_pair<Cfg>(acc, [&](int m, int n, double v0, double v1) {
         int prr = m0 + m, cc = n0 + n;
         if (prr < P2) {
             if (cc < pp) Gr[(int64_t)cc * P2 + prr] = v0;
             if (cc + 1 < pp) Gr[(int64_t)(cc + 1) * P2 + prr] = v1;
         }
     });
+}
+
+// Tile choice for the x contraction: the config with the least padded M x N area.
+enum class XTile { T128, T120 };
+static XTile choose_xtile(int P2, int pp) {
+    auto area = [&](int bm, int bn) {
+        return (double)ceil_div(P2, bm) * bm * ceil_div(pp, bn) * bn;
+    };
+    return area(120, 120) < area(128, 128) ? XTile::T120 : XTile::T128;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -518,11 +515,15 @@ void build_rows(const mg_plan* P, int l2a, int l2b, const int* s, const int* e,
 
 // Batch geometry: K1/K2 work on nb1 rows at a time (H buffer), K3 on nb3 (G buffer).
 static void choose_batches(mg_plan* P) {
+    // Scratch per row: H (run contraction out), S (pair products), G (x contraction out),
+    // R (gathered G).  Budgets are a few GB of the 180 GB HBM: large batches keep every
+    // launch many waves deep (tail < ~2 %) and the launch count low.
     const double hrow = (double)P->p * P->p * P->NxP * 8.0;
-    const double grow = (double)P->P2 * P->p * P->p * 8.0;
-    int nb1 = (int)std::min(1024.0, std::max(16.0, 1.0e9 / hrow));
+    const double srow = (double)P->P2 * P->NxP * 8.0;
+    const double grow = (double)P->P2 * P->p * P->p * 8.0 + (double)P->p * P->nm * 8.0;
+    int nb1 = (int)std::min({2048.0, 6.0e9 / hrow, 4.0e9 / srow});
     nb1 = std::max(16, nb1 / 16 * 16);
-    int nb3 = (int)std::min(2048.0, std::max((double)nb1, 1.5e9 / grow));
+    int nb3 = (int)std::min(8192.0, std::max((double)nb1, 5.0e9 / grow));
     nb3 = std::max(nb1, nb3 / nb1 * nb1);
     P->nb1 = nb1;
     P->nb3 = nb3;
@@ -627,6 +628,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         MG_CUDA(cudaMemsetAsync(P->H.p, 0, P->H.n * sizeof(double), st));
     }
     P->G.ensure((size_t)nb3 * pp * P2);
+    P->S.ensure((size_t)nb1 * P2 * NxP);
     P->R.ensure((size_t)nb3 * ldr);
     P->Sq.ensure((size_t)nb3 * ldq);
     // K-split of the pair contraction so that its grid fills the 148 SMs
@@ -648,13 +650,19 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
 
     static bool attr_done = false;
     const size_t smem_run = RunPipe::smem_bytes;
-    const size_t smem_x = XPipe::smem_bytes;
+    const XTile xt = choose_xtile(P2, pp);
+    const size_t smem_x = xt == XTile::T120 ? XPipeT<CfgX120>::smem_bytes
+                                            : XPipeT<Cfg128>::smem_bytes;
     const size_t smem_pair = PairPipe::smem_bytes;
     if (!attr_done) {
         MG_CUDA(cudaFuncSetAttribute(k_run_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_run));
-        MG_CUDA(cudaFuncSetAttribute(k_x_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_x));
+        MG_CUDA(cudaFuncSetAttribute(k_x_contract<CfgX120>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)XPipeT<CfgX120>::smem_bytes));
+        MG_CUDA(cudaFuncSetAttribute(k_x_contract<Cfg128>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)XPipeT<Cfg128>::smem_bytes));
         MG_CUDA(cudaFuncSetAttribute(k_pair_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_pair));
         attr_done = true;
@@ -691,6 +699,12 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                                  l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p,
                                  P->h2_mode, P->panel.p);
             MG_LAUNCHED();
+            {
+                dim3 gs(ceil_div(P2, PP_CHUNK), nb);
+                k_pair_products<<<gs, 256, 0, st>>>(P->rows.p, (int)b1, P->QT.p, p, P2, NxP,
+                                                    P->l_min, P->S.p);
+                MG_LAUNCHED();
+            }
             dim3 g1(ceil_div((int64_t)p * P->Nxw, CfgRun::BN), tl - tf);
             prof_mark(P, 1, st);
             k_run_contract<<<g1, CfgRun::THREADS, smem_run, st>>>(P->tiles.p + tf, P->poff.p + tf,
@@ -698,13 +712,18 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                                                              P->WQT.p, p, P->Nx, P->Nxw, NxP, cb0,
                                                              cb1, P->H.p);
             MG_LAUNCHED();
-            dim3 g2(ceil_div(pp, CfgX::BN), ceil_div(P2, CfgX::BM), nb);
             prof_mark(P, 2, st);
-            k_x_contract<<<g2, CfgX::THREADS, smem_x, st>>>(P->rows.p, (int)b1, (int)b3, P->QT.p,
-                                                         P->H.p, p, P2, P->Nx, NxP, P->l_min,
-                                                         P->G.p);
+            if (xt == XTile::T120) {
+                dim3 g2(ceil_div(pp, CfgX120::BN), ceil_div(P2, CfgX120::BM), nb);
+                k_x_contract<CfgX120><<<g2, CfgX120::THREADS, smem_x, st>>>(
+                    P->S.p, P->H.p, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->G.p);
+            } else {
+                dim3 g2(ceil_div(pp, Cfg128::BN), ceil_div(P2, Cfg128::BM), nb);
+                k_x_contract<Cfg128><<<g2, Cfg128::THREADS, smem_x, st>>>(
+                    P->S.p, P->H.p, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->G.p);
+            }
             MG_LAUNCHED();
-            launches += 3 + (dt1 ? 1 : 0);
+            launches += 4 + (dt1 ? 1 : 0);
             for (int64_t r = b1; r < e1; ++r) {
                 double m = (double)(hrows[r].jhi - hrows[r].jlo + 1);
                 f_run += 2.0 * p * p * P->Nx * m;

@@ -32,7 +32,7 @@ struct mg_plan {
     mg::DBuf<double> q, QT, WQT, C, v, lf, wr2;
     mg::DBuf<int> modes;  // [nm][3]
     // scratch
-    mg::DBuf<double> ZT, panel, H, G, R, Sq, Z, gamma;
+    mg::DBuf<double> ZT, panel, H, S, G, R, Sq, Z, gamma;
     mg::DBuf<int64_t> poff;
     mg::DBuf<MgRow> rows;
     mg::DBuf<int64_t> zoff;

@@ -78,7 +78,7 @@ class GammaPlan:
     def kernel_ms(self) -> dict:
         ms = np.zeros(6)
         nat.check(nat.lib().mg_plan_kernel_ms(self._h, nat.ptr(ms)))
-        return dict(zip(("panels", "run", "x", "gather", "pair", "final"), ms.tolist()))
+        return dict(zip(("operands", "run", "x", "gather", "pair", "final"), ms.tolist()))
 
     def close(self):
         if self._h:

@@ -220,3 +220,23 @@ class TestGammaLarge:
         assert frob_rel(sum(parts), full) < 1e-12
         plan.execute()
         assert np.array_equal(plan.fetch(), full)              # bitwise reproducible
+
+
+@pytest.mark.parametrize("cfg,ntri", [("c2", 1500), ("c4", 160)])
+def test_large_config_partials(cfg, ntri):
+    """Configs 2 and 4 (p = 22, 30: several M-tiles in the x/pair contractions, packed
+    slots spanning rows): flat-range partials at 30 % and 80 % of the index vs the oracle on
+    the same GPU-built q̃."""
+    from paper_1503_08809_b200 import build_qtilde
+    hi = host_inputs(cfg)
+    C, qt = build_qtilde(hi)
+    t = BasisTables(hi.q, qt, C, hi.v, 2, hi.l_max)
+    m = ModeMapping(hi.entries, hi.spec.p)
+    total = domain_count(2, hi.l_max)
+    for frac in (0.3, 0.8):
+        a = int(frac * total)
+        got = gamma3d_matrix(t, m, RadialGrid(hi.x),
+                             domain=DomainRange(2, hi.l_max, a, a + ntri)).values
+        want = ref.gamma3d(hi.q, qt, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max, a, a + ntri,
+                           workers=8, block=8)
+        assert frob_rel(got, want) < 1e-10
