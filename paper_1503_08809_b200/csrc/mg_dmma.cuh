@@ -110,6 +110,7 @@ enum class ASrc { KMajor, MMajor, Raw };
 // Stage layout: [A tile (absent for Raw)][B tile][raw (kRaw doubles)].
 template <class Cfg, int BK, int STAGES, ASrc AS, bool BKM, int kRaw>
 struct Pipe {
+    static constexpr int THREADS = Cfg::THREADS;
     static constexpr int SA = AS == ASrc::Raw ? 0 : tile_doubles(AS == ASrc::KMajor, Cfg::BM, BK);
     static constexpr int SB = tile_doubles(BKM, Cfg::BN, BK);
     static constexpr int SS = SA + SB + kRaw;
@@ -185,6 +186,240 @@ struct Pipe {
             }
         }
         cp_async_wait<0>();
+    }
+};
+
+
+// ------------------------------------------------------------------------------------------
+// Warp-specialised variant: Cfg::WARPS consumer warps + 1 producer warp.  The producer
+// streams every stage with cp.async and signals a per-stage "full" mbarrier through
+// cp.async.mbarrier.arrive.noinc; consumers wait on "full", run the DMMAs, and release the
+// stage through an "empty" mbarrier (one arrive per consumer warp).  No CTA-wide barrier in
+// the main loop, and the consumers never execute copy/address code.
+// Producer contract: __device__ void issue_warp(int kt, double* As, double* Bs, int lane) const;
+//                    __device__ int kvalid_last() const;
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(
+        smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, int parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        " WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity));
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)));
+}
+
+// single-warp tile copies (the producer warp): same layouts as copy_kmajor / copy_mmajor
+template <int BK, int W, class RowPtr>
+__device__ __forceinline__ void warp_copy_kmajor(double* dst, RowPtr&& src_row, int w_valid,
+                                                 int lane) {
+    constexpr int CPR = W / 2, CH = BK * CPR;
+#pragma unroll 4
+    for (int c = lane; c < CH; c += 32) {
+        int k = c / CPR, m = (c % CPR) * 2;
+        const double* s = src_row(k);
+        double* d = dst + k * ld_kmajor(W) + m;
+        int bytes = (s && m < w_valid) ? ((w_valid - m) >= 2 ? 16 : 8) : 0;
+        cp_async16(d, bytes ? s + m : d, bytes);
+    }
+}
+template <int BK, int W, class RowPtr>
+__device__ __forceinline__ void warp_copy_mmajor(double* dst, RowPtr&& src_row, int k_valid,
+                                                 int lane) {
+    constexpr int CPR = BK / 2, CH = W * CPR;
+#pragma unroll 4
+    for (int c = lane; c < CH; c += 32) {
+        int m = c / CPR, k = (c % CPR) * 2;
+        const double* s = src_row(m);
+        double* d = dst + m * ld_mmajor(BK) + k;
+        int bytes = (s && k < k_valid) ? ((k_valid - k) >= 2 ? 16 : 8) : 0;
+        cp_async16(d, bytes ? s + k : d, bytes);
+    }
+}
+
+template <class Cfg, int BK, int STAGES, bool AK, bool BKM>
+struct PipeWS {
+    static constexpr int WARPS = Cfg::WARPS_M * Cfg::WARPS_N;
+    static constexpr int THREADS = Cfg::THREADS + 32;
+    static constexpr int SA = tile_doubles(AK, Cfg::BM, BK);
+    static constexpr int SB = tile_doubles(BKM, Cfg::BN, BK);
+    static constexpr int SS = SA + SB;
+    static constexpr size_t smem_bytes = (size_t)STAGES * SS * sizeof(double) + 2 * STAGES * 8;
+
+    __device__ static bool is_producer() { return (int)(threadIdx.x >> 5) == WARPS; }
+
+    // Returns true in consumer threads (which then own `acc`); the producer returns false.
+    template <class Prod>
+    __device__ static bool run(int ktiles, const Prod& prod, double* smem, Acc<Cfg>& acc) {
+        constexpr int FM = Cfg::FM, FN = Cfg::FN;
+        uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SS);
+        uint64_t* empty = full + STAGES;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(full + s, 32);
+                mbar_init(empty + s, WARPS);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        }
+        __syncthreads();
+        if (warp == WARPS) {  // ---------------- producer warp
+            for (int kt = 0; kt < ktiles; ++kt) {
+                const int s = kt % STAGES;
+                if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
+                double* st = smem + s * SS;
+                prod.issue_warp(kt, st, st + SA, lane);
+                cp_async_mbar_arrive(full + s);
+            }
+            cp_async_wait<0>();
+            return false;
+        }
+        // ------------------------------------------------------------- consumer warps
+        const int g = lane >> 2, t = lane & 3;
+        const int wm = (warp / Cfg::WARPS_N) * (8 * FM), wn = (warp % Cfg::WARPS_N) * (8 * FN);
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
+        for (int kt = 0; kt < ktiles; ++kt) {
+            const int s = kt % STAGES;
+            mbar_wait(full + s, (kt / STAGES) & 1);
+            const double* As = smem + s * SS;
+            const double* Bs = As + SA;
+            double a[2][FM], b[2][FN];
+            auto load_frags = [&](int buf, int k) {
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi) a[buf][mi] = frag_ld<AK, Cfg::BM, BK>(As, k, wm + mi * 8 + g);
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni) b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g);
+            };
+            const int nks = kt + 1 < ktiles ? BK / 4 : (prod.kvalid_last() + 3) / 4;
+            load_frags(0, t);
+#pragma unroll
+            for (int ks = 0; ks < BK / 4; ++ks) {
+                if (ks < nks) {
+                    const int cur = ks & 1;
+                    if (ks + 1 < BK / 4) load_frags(cur ^ 1, (ks + 1) * 4 + t);
+#pragma unroll
+                    for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                        for (int ni = 0; ni < FN; ++ni)
+                            dmma884(acc.c[mi][ni], a[cur][mi], b[cur][ni]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+        return true;
+    }
+};
+
+
+// ------------------------------------------------------------------------------------------
+// Bulk-copy (TMA engine) variant of the warp-specialised pipeline.  The producer warp moves
+// whole contiguous rows with cp.async.bulk (one instruction per row, SASS UBLKCP) completing
+// on the stage's "full" mbarrier by transaction bytes (expect_tx), so a stage costs ~64-240
+// copy instructions instead of thousands of 16-byte cp.async chunks.  No zero fill: the
+// producers arrange that rows/columns outside the matrix are either real zeros (padded
+// panels) or only feed accumulator rows/columns the epilogue discards.
+// Producer contract: __device__ void bulk_rows(int kt, double* As, double* Bs, int lane,
+//                        uint64_t* bar) const;   // issues the copies, all 32 lanes
+//                    __device__ uint32_t stage_bytes(int kt) const;  // total bytes of stage kt
+//                    __device__ int kvalid_last() const;
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
+                 ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <class Cfg, int BK, int STAGES, bool AK, bool BKM>
+struct PipeTMA {
+    static constexpr int WARPS = Cfg::WARPS_M * Cfg::WARPS_N;
+    static constexpr int THREADS = Cfg::THREADS + 32;
+    static constexpr int SA = tile_doubles(AK, Cfg::BM, BK);
+    static constexpr int SB = tile_doubles(BKM, Cfg::BN, BK);
+    static constexpr int SS = SA + SB;
+    static constexpr size_t smem_bytes = (size_t)STAGES * SS * sizeof(double) + 2 * STAGES * 8;
+
+    template <class Prod>
+    __device__ static bool run(int ktiles, const Prod& prod, double* smem, Acc<Cfg>& acc) {
+        constexpr int FM = Cfg::FM, FN = Cfg::FN;
+        uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SS);
+        uint64_t* empty = full + STAGES;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(full + s, 1);
+                mbar_init(empty + s, WARPS);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        }
+        __syncthreads();
+        if (warp == WARPS) {  // ---------------- producer warp
+            for (int kt = 0; kt < ktiles; ++kt) {
+                const int s = kt % STAGES;
+                if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
+                if (lane == 0) mbar_arrive_expect_tx(full + s, prod.stage_bytes(kt));
+                __syncwarp();
+                double* st = smem + s * SS;
+                prod.bulk_rows(kt, st, st + SA, lane, full + s);
+            }
+            return false;
+        }
+        // ------------------------------------------------------------- consumer warps
+        const int g = lane >> 2, t = lane & 3;
+        const int wm = (warp / Cfg::WARPS_N) * (8 * FM), wn = (warp % Cfg::WARPS_N) * (8 * FN);
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
+        for (int kt = 0; kt < ktiles; ++kt) {
+            const int s = kt % STAGES;
+            mbar_wait(full + s, (kt / STAGES) & 1);
+            const double* As = smem + s * SS;
+            const double* Bs = As + SA;
+            double a[2][FM], b[2][FN];
+            auto load_frags = [&](int buf, int k) {
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi) a[buf][mi] = frag_ld<AK, Cfg::BM, BK>(As, k, wm + mi * 8 + g);
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni) b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g);
+            };
+            const int nks = kt + 1 < ktiles ? BK / 4 : (prod.kvalid_last() + 3) / 4;
+            load_frags(0, t);
+#pragma unroll
+            for (int ks = 0; ks < BK / 4; ++ks) {
+                if (ks < nks) {
+                    const int cur = ks & 1;
+                    if (ks + 1 < BK / 4) load_frags(cur ^ 1, (ks + 1) * 4 + t);
+#pragma unroll
+                    for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                        for (int ni = 0; ni < FN; ++ni)
+                            dmma884(acc.c[mi][ni], a[cur][mi], b[cur][ni]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+        return true;
     }
 };
 

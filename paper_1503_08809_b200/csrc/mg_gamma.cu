@@ -19,6 +19,7 @@
 // is owned by exactly one CTA per launch and rows are reduced in a fixed order, so a run is
 // bitwise reproducible.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -28,14 +29,21 @@
 
 namespace mg {
 
+constexpr int RUN_TN = 120;             // run-contraction N tile ((c', x) columns)
+constexpr int RUN_LDB = RUN_TN + 4;     // smem-identical row stride of WQB / A panels
+
 // ------------------------------------------------------------------------------------------
 // setup kernels
 // ------------------------------------------------------------------------------------------
 
-// QT[l][c][x] = q̃[c][x][l] ; WQT[cls(l)][c][x] = wr2[x] q̃[c][x][l]  (x zero-padded to NxP)
+// QT[l][c][x] = q̃[c][x][l]  (x zero-padded to NxP), and the run contraction's B operand
+// WQB: for parity class par, column block nb of RUN_TN columns n = c*Nxw + x,
+//   WQB[base[par] + (nb*Rpar + j)*RUN_LDB + n%RUN_TN] = wr2[x] q̃[c][x][l],  l = l0(par) + 2j
+// (Rpar = class size + RUN_BK zero rows; smem-identical rows, so a stage is one bulk copy)
 __global__ void k_transpose_qt(const double* __restrict__ qt, const double* __restrict__ wr2,
-                               int p, int Nx, int NxP, int Nxw, int L, int l_min, int l0_1,
-                               int n0, double* __restrict__ QT, double* __restrict__ WQT) {
+                               int p, int Nx, int NxP, int Nxw, int L, int l_min,
+                               longlong2 wbase, int2 wrows, double* __restrict__ QT,
+                               double* __restrict__ WQT) {
     int64_t total = (int64_t)L * p * NxP;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -45,9 +53,14 @@ __global__ void k_transpose_qt(const double* __restrict__ qt, const double* __re
         int li = (int)(r / p);
         double val = x < Nx ? qt[((int64_t)c * Nx + x) * L + li] : 0.0;
         QT[i] = val;
-        int l = l_min + li;
-        int s = ((l ^ l_min) & 1) == 0 ? (l - l_min) / 2 : n0 + (l - l0_1) / 2;
-        if (x < Nxw) WQT[((int64_t)s * p + c) * Nxw + x] = x < Nx ? wr2[x] * val : 0.0;
+        const int l = l_min + li, par = l & 1;
+        const int j = (l - (l_min + ((l_min ^ par) & 1))) / 2;
+        if (x < Nxw) {
+            const int n = c * Nxw + x, nb = n / RUN_TN;
+            const int64_t o = (par ? wbase.y : wbase.x) +
+                              ((int64_t)nb * (par ? wrows.y : wrows.x) + j) * RUN_LDB + n % RUN_TN;
+            WQT[o] = x < Nx ? wr2[x] * val : 0.0;
+        }
     }
 }
 
@@ -71,20 +84,17 @@ __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t*
 // ------------------------------------------------------------------------------------------
 constexpr int RUN_BK = 32, RUN_ST = 3;
 constexpr int X_BK = 32;
+constexpr int X_LDK = X_BK + 4;  // x-blocked S/H row stride: [row][x/32][m][36], smem-identical
 constexpr int PAIR_BK = 32, PAIR_ST = 3;
-using Cfg128 = TileCfg<2, 4, 8, 4>;  // 128 x 128, 8 warps, 64 accumulators per lane
-#ifndef MG_RUN_WIDE
-#define MG_RUN_WIDE 1
-#endif
-#if MG_RUN_WIDE
-using CfgRun = TileCfg<4, 4, 4, 4>;  // 128 x 128, 16 warps, 32 accumulators per lane
-#else
-using CfgRun = Cfg128;
-#endif
-using RunPipe = Pipe<CfgRun, RUN_BK, RUN_ST, ASrc::KMajor, true, 0>;
+using Cfg128 = TileCfg<2, 4, 8, 4>;   // 128 x 128, 8 warps, 64 accumulators per lane
+using CfgX120 = TileCfg<5, 3, 3, 5>;  // 120 x 120, 15 warps, 30 accumulators per lane
+using CfgRun = CfgX120;                // run contraction: 15 consumer warps + 1 producer
+using RunPipe = PipeTMA<CfgRun, RUN_BK, RUN_ST, true, true>;
 using PairPipe = Pipe<Cfg128, PAIR_BK, PAIR_ST, ASrc::KMajor, true, 0>;
-constexpr int GB_M = 128;
-
+constexpr int RUN_TM = CfgRun::BM;     // (row, c) slots per run tile = A panel width
+static_assert(RUN_TN == CfgRun::BN && RUN_LDB == ld_kmajor(RUN_TM) &&
+                  RUN_LDB == ld_kmajor(RUN_TN) && RUN_BK == 32,
+              "bulk-copied run tiles must match the shared-memory layout");
 constexpr int PANEL_THREADS = 256;
 constexpr int PANEL_JC = 32;  // j values per shared-memory weight chunk
 
@@ -119,8 +129,8 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
         }
         __syncthreads();
         // 2) panel[j][slot] = zm(row(slot), j) * q_c(slot)(l1(j)), slot-contiguous stores
-        for (int e = threadIdx.x; e < PANEL_JC * GB_M; e += PANEL_THREADS) {
-            const int jl = e / GB_M, slot = e % GB_M;
+        for (int e = threadIdx.x; e < PANEL_JC * RUN_TM; e += PANEL_THREADS) {
+            const int jl = e / RUN_TM, slot = e % RUN_TM;
             if (jc + jl >= kt) break;
             double val = 0.0;
             if (slot < tl.nslots) {
@@ -131,7 +141,7 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
                     val = z * q[(int64_t)c * L + (l1 - l_min)];
                 }
             }
-            out[(int64_t)(jc + jl) * GB_M + slot] = val;
+            out[(int64_t)(jc + jl) * RUN_LDB + slot] = val;
         }
         __syncthreads();
     }
@@ -143,26 +153,29 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
 //   even); H rows are [c'][NxP] (x padded to the x-contraction's BK, pads stay zero).
 // ------------------------------------------------------------------------------------------
 struct RunProd {
-    const double* panel;  // this tile's panel
-    const double* wqt;    // WQT + cls*ldb + n0
-    int64_t ldb;
-    int jlo, jhi, n_valid, kv_last;
+    const double* panel;  // this tile's A panel, rows of RUN_LDB doubles
+    const double* wqb;    // WQB rows of this (parity class, column block), from row jlo
+    int n_valid, kv_last;
     __device__ int kvalid_last() const { return kv_last; }
-    __device__ void issue(int kt, double* As, double* Bs, double*) const {
-        copy_kmajor<RUN_BK, 128, CfgRun::THREADS>(
-            As, [&](int k) { return panel + (int64_t)(kt * RUN_BK + k) * GB_M; }, GB_M);
-        copy_kmajor<RUN_BK, 128, CfgRun::THREADS>(Bs, [&](int k) -> const double* {
-            int j = jlo + kt * RUN_BK + k;
-            return j <= jhi ? wqt + (int64_t)j * ldb : nullptr;
-        }, n_valid);
+    __device__ uint32_t stage_bytes(int) const {
+        return 2 * RUN_BK * RUN_LDB * (uint32_t)sizeof(double);
+    }
+    // two bulk copies: 32 panel rows and 32 WQB rows (zero rows pad every class's end)
+    __device__ void bulk_rows(int kt, double* As, double* Bs, int lane, uint64_t* bar) const {
+        if (lane == 0)
+            bulk_g2s(As, panel + (int64_t)kt * RUN_BK * RUN_LDB,
+                     RUN_BK * RUN_LDB * sizeof(double), bar);
+        else if (lane == 1)
+            bulk_g2s(Bs, wqb + (int64_t)kt * RUN_BK * RUN_LDB,
+                     RUN_BK * RUN_LDB * sizeof(double), bar);
     }
 };
 
-__global__ void __launch_bounds__(CfgRun::THREADS, 1)
+__global__ void __launch_bounds__(RunPipe::THREADS, 1)
 k_run_contract(const MgTile* __restrict__ tiles, const int64_t* __restrict__ poff,
                const double* __restrict__ panel, int row_base, const MgRow* __restrict__ rows,
-               const double* __restrict__ WQT, int p, int Nx, int Nxw, int NxP, int cbase0,
-               int cbase1, double* __restrict__ H) {
+               const double* __restrict__ WQB, int p, int Nx, int Nxw, int NxP,
+               longlong2 wbase, int2 wrows, double* __restrict__ H) {
     extern __shared__ __align__(16) double smem[];
     const MgTile tl = tiles[blockIdx.y];
     const int n0 = blockIdx.x * CfgRun::BN;
@@ -171,21 +184,21 @@ k_run_contract(const MgTile* __restrict__ tiles, const int64_t* __restrict__ pof
     const int nk = tl.jhi - tl.jlo + 1;
     RunProd pr;
     pr.panel = panel + poff[blockIdx.y];
-    pr.wqt = WQT + (int64_t)(par ? cbase1 : cbase0) * ldb + n0;
-    pr.ldb = ldb;
-    pr.jlo = tl.jlo;
-    pr.jhi = tl.jhi;
+    pr.wqb = WQB + (par ? wbase.y : wbase.x) +
+             ((int64_t)blockIdx.x * (par ? wrows.y : wrows.x) + tl.jlo) * RUN_LDB;
     pr.n_valid = (int)(ldb - n0 < CfgRun::BN ? ldb - n0 : CfgRun::BN);
     pr.kv_last = nk - (nk - 1) / RUN_BK * RUN_BK;
     Acc<CfgRun> acc;
-    RunPipe::run((nk + RUN_BK - 1) / RUN_BK, pr, smem, acc);
+    if (!RunPipe::run((nk + RUN_BK - 1) / RUN_BK, pr, smem, acc)) return;  // producer warp
     const int64_t hbase = (int64_t)(tl.row0 - row_base) * p + tl.c0;  // H row of slot 0
-    const int64_t ldh = (int64_t)p * NxP;
     acc_foreach_pair<CfgRun>(acc, [&](int m, int n, double v0, double v1) {
         const int gn = n0 + n;
         if (m < tl.nslots && gn < ldb) {
             const int cp = gn / Nxw, x = gn - cp * Nxw;   // Nxw even: (gn, gn+1) share c'
-            double* h = H + (hbase + m) * ldh + (int64_t)cp * NxP + x;
+            const int64_t slot = hbase + m, rr = slot / p;
+            const int c = (int)(slot - rr * p);
+            double* h = H + ((rr * (NxP / X_BK) + x / X_BK) * (p * p) + c * p + cp) * X_LDK +
+                        (x & (X_BK - 1));
             if (x + 1 < Nx) {
                 *reinterpret_cast<double2*>(h) = make_double2(v0, v1);
             } else if (x < Nx) {
@@ -222,7 +235,7 @@ k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __rest
     const MgRow rw = rows[row_b1 + r];
     const double2* q2 = reinterpret_cast<const double2*>(QT + (int64_t)(rw.l2 - l_min) * p * NxP);
     const double2* q3 = reinterpret_cast<const double2*>(QT + (int64_t)(rw.l3 - l_min) * p * NxP);
-    double2* out = reinterpret_cast<double2*>(S + (int64_t)r * P2 * NxP);
+    double* out = S + (int64_t)r * P2 * (NxP / X_BK) * X_LDK;
     const int nx2 = NxP / 2;
     int pr = blockIdx.x * PP_CHUNK, a, b;
     pair_of(pr, a, b);
@@ -233,34 +246,57 @@ k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __rest
         const double2* b3 = q3 + b * nx2;
         for (int x = threadIdx.x; x < nx2; x += blockDim.x) {
             double2 u = a2[x], w = b3[x], y = b2[x], z = a3[x];
-            out[(int64_t)pr * nx2 + x] = make_double2(u.x * w.x + y.x * z.x, u.y * w.y + y.y * z.y);
+            const int xx = 2 * x;
+            *reinterpret_cast<double2*>(out + ((int64_t)(xx / X_BK) * P2 + pr) * X_LDK +
+                                        (xx & (X_BK - 1))) =
+                make_double2(u.x * w.x + y.x * z.x, u.y * w.y + y.y * z.y);
         }
         if (++a > b) { ++b; a = 0; }  // next pair in b-major order
     }
 }
 
-using CfgX120 = TileCfg<5, 3, 3, 5>;  // 120 x 120, 15 warps, 30 accumulators per lane
 template <class Cfg>
-using XPipeT = Pipe<Cfg, X_BK, 3, ASrc::MMajor, false, 0>;
+struct XPipeSel {
+    using type = Pipe<Cfg, X_BK, 3, ASrc::MMajor, false, 0>;
+};
+template <>
+struct XPipeSel<CfgX120> {
+    using type = PipeTMA<CfgX120, X_BK, 3, false, false>;
+};
+template <class Cfg>
+using XPipeT = typename XPipeSel<Cfg>::type;
 
 template <class Cfg>
 struct XProd {
-    const double* s;   // S row block of this CTA: S[r] + m0*NxP
-    const double* h;   // H row block: H[r] + n0*NxP
-    int NxP, m_valid, n_valid, kv_last;
+    const double* s;   // S + (r*XB*P2 + m0)*X_LDK     (x-blocked, block stride P2*X_LDK)
+    const double* h;   // H + (r*XB*pp + n0)*X_LDK     (x-blocked, block stride pp*X_LDK)
+    int64_t sblk, hblk;
+    int m_valid, n_valid, kv_last;
     __device__ int kvalid_last() const { return kv_last; }
     __device__ void issue(int kt, double* As, double* Bs, double*) const {
+        const double* sa = s + kt * sblk;
+        const double* hb = h + kt * hblk;
         copy_mmajor<X_BK, Cfg::BM, Cfg::THREADS>(As, [&](int m) -> const double* {
-            return m < m_valid ? s + (int64_t)m * NxP + kt * X_BK : nullptr;
+            return m < m_valid ? sa + (int64_t)m * X_LDK : nullptr;
         }, X_BK);
         copy_mmajor<X_BK, Cfg::BN, Cfg::THREADS>(Bs, [&](int m) -> const double* {
-            return m < n_valid ? h + (int64_t)m * NxP + kt * X_BK : nullptr;
+            return m < n_valid ? hb + (int64_t)m * X_LDK : nullptr;
         }, X_BK);
+    }
+    __device__ uint32_t stage_bytes(int) const {
+        return (m_valid + n_valid) * X_LDK * (uint32_t)sizeof(double);
+    }
+    // one bulk copy per operand: the x-blocked global layout equals the smem tile layout
+    __device__ void bulk_rows(int kt, double* As, double* Bs, int lane, uint64_t* bar) const {
+        if (lane == 0)
+            bulk_g2s(As, s + kt * sblk, m_valid * X_LDK * sizeof(double), bar);
+        else if (lane == 1)
+            bulk_g2s(Bs, h + kt * hblk, n_valid * X_LDK * sizeof(double), bar);
     }
 };
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, 1)
+__global__ void __launch_bounds__(XPipeT<Cfg>::THREADS, 1)
 k_x_contract(const double* __restrict__ S, const double* __restrict__ H, int row_b1,
              int row_b3, int p, int P2, int Nx, int NxP, double* __restrict__ G) {
     extern __shared__ __align__(16) double smem[];
@@ -268,14 +304,20 @@ k_x_contract(const double* __restrict__ S, const double* __restrict__ H, int row
     const int m0 = blockIdx.y * Cfg::BM, n0 = blockIdx.x * Cfg::BN;
     const int pp = p * p;
     XProd<Cfg> pr;
-    pr.s = S + ((int64_t)r * P2 + m0) * NxP;
-    pr.h = H + ((int64_t)r * pp + n0) * NxP;
-    pr.NxP = NxP;
+    const int XB = NxP / X_BK;
+    pr.s = S + ((int64_t)r * XB * P2 + m0) * X_LDK;
+    pr.h = H + ((int64_t)r * XB * pp + n0) * X_LDK;
+    pr.sblk = (int64_t)P2 * X_LDK;
+    pr.hblk = (int64_t)pp * X_LDK;
     pr.m_valid = min(Cfg::BM, P2 - m0);
     pr.n_valid = min(Cfg::BN, pp - n0);
     pr.kv_last = Nx - (NxP / X_BK - 1) * X_BK;
     Acc<Cfg> acc;
-    XPipeT<Cfg>::run(NxP / X_BK, pr, smem, acc);
+    if constexpr (std::is_same_v<XPipeT<Cfg>, Pipe<Cfg, X_BK, 3, ASrc::MMajor, false, 0>>) {
+        XPipeT<Cfg>::run(NxP / X_BK, pr, smem, acc);
+    } else {
+        if (!XPipeT<Cfg>::run(NxP / X_BK, pr, smem, acc)) return;  // producer warp
+    }
     double* Gr = G + (int64_t)(row_b1 + r - row_b3) * pp * P2;
     acc_foreach_pair<Cfg>(acc, [&](int m, int n, double v0, double v1) {
         int prr = m0 + m, cc = n0 + n;
@@ -462,20 +504,20 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
         qt_src = staged.p;
     }
     P->QT.alloc((size_t)L * p * P->NxP);
-    P->WQT.alloc((size_t)L * p * P->Nxw);
-    // classes: even-parity l first when l_min is even (class of l_min is class 0 in storage)
-    // storage index s(l) = (l - l_min)/2 for the parity of l_min, n0 + (l - l0')/2 otherwise
-    int n0 = (L + 1) / 2;
+    const int nb = ceil_div((int64_t)p * P->Nxw, RUN_TN);
+    for (int par = 0; par < 2; ++par) P->wrows[par] = P->nclass[par] + RUN_BK;
+    P->wbase[0] = 0;
+    P->wbase[1] = (int64_t)nb * P->wrows[0] * RUN_LDB;
+    const size_t wsize = (size_t)nb * (P->wrows[0] + P->wrows[1]) * RUN_LDB;
+    P->WQT.alloc(wsize);
+    MG_CUDA(cudaMemset(P->WQT.p, 0, wsize * sizeof(double)));
     k_transpose_qt<<<1184, 256>>>(qt_src, P->wr2.p, p, Nx, P->NxP, P->Nxw, L, l_min,
-                                  l_min + 1, n0, P->QT.p, P->WQT.p);
+                                  make_longlong2(P->wbase[0], P->wbase[1]),
+                                  make_int2(P->wrows[0], P->wrows[1]), P->QT.p, P->WQT.p);
     MG_LAUNCHED();
     MG_CUDA(cudaDeviceSynchronize());
 }
 
-// Storage class offset (in l-slots) of parity `par` inside WQT.
-static inline int class_base(const mg_plan* P, int par) {
-    return par == (P->l_min & 1) ? 0 : (P->L + 1) / 2;
-}
 
 static inline bool lex_ge(int a2, int a3, int b2, int b3) {
     return a2 > b2 || (a2 == b2 && a3 >= b3);
@@ -585,9 +627,9 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             int64_t g1 = g0;
             while (g1 < e1 && hrows[g1].l2 == hrows[g0].l2 && hrows[g1].par == hrows[g0].par) ++g1;
             const int64_t nsl = (g1 - g0) * p;
-            for (int64_t s0 = 0; s0 < nsl; s0 += GB_M) {
+            for (int64_t s0 = 0; s0 < nsl; s0 += RUN_TM) {
                 MgTile t;
-                const int64_t s1 = std::min<int64_t>(s0 + GB_M, nsl);
+                const int64_t s1 = std::min<int64_t>(s0 + RUN_TM, nsl);
                 t.row0 = (int)(g0 + s0 / p);
                 t.c0 = (int)(s0 % p);
                 t.nslots = (int)(s1 - s0);
@@ -603,7 +645,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                 max_tile_rows = std::max(max_tile_rows, t.nrows);
                 tiles.push_back(t);
                 poff.push_back(off);
-                off += round_up(t.jhi - t.jlo + 1, RUN_BK) * GB_M;
+                off += round_up(t.jhi - t.jlo + 1, RUN_BK) * RUN_LDB;
             }
             g0 = g1;
         }
@@ -623,12 +665,13 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     }
     if (dt1) P->ZT.ensure(maxzt);
     P->panel.ensure(maxpanel);
-    if (P->H.n < (size_t)nb1 * pp * NxP) {  // x pads of H are never written: zero them once
-        P->H.ensure((size_t)nb1 * pp * NxP);
+    const size_t hsize = (size_t)nb1 * pp * (NxP / X_BK) * X_LDK;
+    if (P->H.n < hsize) {  // x pads of H are never written: zero them once
+        P->H.ensure(hsize);
         MG_CUDA(cudaMemsetAsync(P->H.p, 0, P->H.n * sizeof(double), st));
     }
     P->G.ensure((size_t)nb3 * pp * P2);
-    P->S.ensure((size_t)nb1 * P2 * NxP);
+    P->S.ensure((size_t)nb1 * P2 * (NxP / X_BK) * X_LDK);
     P->R.ensure((size_t)nb3 * ldr);
     P->Sq.ensure((size_t)nb3 * ldq);
     // K-split of the pair contraction so that its grid fills the 148 SMs
@@ -672,7 +715,6 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
 
     double f_run = 0, f_x = 0, f_pair = 0;
     int64_t launches = 0;
-    const int cb0 = class_base(P, 0), cb1 = class_base(P, 1);
     int bidx = 0;
     for (int64_t b3 = 0; b3 < nrows; b3 += nb3) {
         int64_t e3 = std::min<int64_t>(b3 + nb3, nrows);
@@ -707,19 +749,21 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             }
             dim3 g1(ceil_div((int64_t)p * P->Nxw, CfgRun::BN), tl - tf);
             prof_mark(P, 1, st);
-            k_run_contract<<<g1, CfgRun::THREADS, smem_run, st>>>(P->tiles.p + tf, P->poff.p + tf,
+            k_run_contract<<<g1, RunPipe::THREADS, smem_run, st>>>(P->tiles.p + tf, P->poff.p + tf,
                                                              P->panel.p, (int)b1, P->rows.p,
-                                                             P->WQT.p, p, P->Nx, P->Nxw, NxP, cb0,
-                                                             cb1, P->H.p);
+                                                             P->WQT.p, p, P->Nx, P->Nxw, NxP,
+                                                             make_longlong2(P->wbase[0], P->wbase[1]),
+                                                             make_int2(P->wrows[0], P->wrows[1]),
+                                                             P->H.p);
             MG_LAUNCHED();
             prof_mark(P, 2, st);
             if (xt == XTile::T120) {
                 dim3 g2(ceil_div(pp, CfgX120::BN), ceil_div(P2, CfgX120::BM), nb);
-                k_x_contract<CfgX120><<<g2, CfgX120::THREADS, smem_x, st>>>(
+                k_x_contract<CfgX120><<<g2, XPipeT<CfgX120>::THREADS, smem_x, st>>>(
                     P->S.p, P->H.p, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->G.p);
             } else {
                 dim3 g2(ceil_div(pp, Cfg128::BN), ceil_div(P2, Cfg128::BM), nb);
-                k_x_contract<Cfg128><<<g2, Cfg128::THREADS, smem_x, st>>>(
+                k_x_contract<Cfg128><<<g2, XPipeT<Cfg128>::THREADS, smem_x, st>>>(
                     P->S.p, P->H.p, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->G.p);
             }
             MG_LAUNCHED();

@@ -28,6 +28,8 @@ struct mg_plan {
     int P2 = 0;        // p(p+1)/2 unordered basis pairs
     int Nxw = 0;       // x stride of WQT rows (Nx when even, else NxP)
     int l0[2] = {0, 0};      // first l of each parity class
+    int64_t wbase[2] = {0, 0};  // WQB offset of each parity class
+    int wrows[2] = {0, 0};      // WQB rows per column block of each class (+ zero rows)
     int nclass[2] = {0, 0};  // number of l in each parity class
     mg::DBuf<double> q, QT, WQT, C, v, lf, wr2;
     mg::DBuf<int> modes;  // [nm][3]
