@@ -423,6 +423,98 @@ struct PipeTMA {
     }
 };
 
+
+// Persistent form of PipeTMA: the CTA walks work items it = first, first + stride, ... and
+// the producer keeps streaming the next item's stages while the consumers finish the current
+// item and run its epilogue, so per-item pipeline fill is hidden.
+// Item producer contract: int ktiles(int it); uint32_t stage_bytes(int it, int kt);
+//   void bulk_rows(int it, int kt, double* As, double* Bs, int lane, uint64_t* bar);
+//   int kvalid_last(int it);   and the consumer epilogue epi(it, acc).
+template <class Cfg, int BK, int STAGES, bool AK, bool BKM>
+struct PipeTMAPersistent {
+    using Base = PipeTMA<Cfg, BK, STAGES, AK, BKM>;
+    static constexpr int WARPS = Base::WARPS, THREADS = Base::THREADS;
+    static constexpr int SA = Base::SA, SB = Base::SB, SS = Base::SS;
+    static constexpr size_t smem_bytes = Base::smem_bytes;
+
+    template <class Prod, class Epi>
+    __device__ static void run(int first, int stride, int nitems, const Prod& prod, Epi&& epi,
+                               double* smem) {
+        constexpr int FM = Cfg::FM, FN = Cfg::FN;
+        uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SS);
+        uint64_t* empty = full + STAGES;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(full + s, 1);
+                mbar_init(empty + s, WARPS);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        }
+        __syncthreads();
+        if (warp == WARPS) {  // ---------------- producer warp
+            int g = 0;
+            for (int it = first; it < nitems; it += stride) {
+                const int kts = prod.ktiles(it);
+                for (int kt = 0; kt < kts; ++kt, ++g) {
+                    const int s = g % STAGES;
+                    if (g >= STAGES) mbar_wait(empty + s, ((g / STAGES) - 1) & 1);
+                    if (lane == 0) mbar_arrive_expect_tx(full + s, prod.stage_bytes(it, kt));
+                    __syncwarp();
+                    double* st = smem + s * SS;
+                    prod.bulk_rows(it, kt, st, st + SA, lane, full + s);
+                }
+            }
+            return;
+        }
+        // ------------------------------------------------------------- consumer warps
+        const int g4 = lane >> 2, t = lane & 3;
+        const int wm = (warp / Cfg::WARPS_N) * (8 * FM), wn = (warp % Cfg::WARPS_N) * (8 * FN);
+        Acc<Cfg> acc;
+        int g = 0;
+        for (int it = first; it < nitems; it += stride) {
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
+            const int kts = prod.ktiles(it);
+            const int kvl = prod.kvalid_last(it);
+            for (int kt = 0; kt < kts; ++kt, ++g) {
+                const int s = g % STAGES;
+                mbar_wait(full + s, (g / STAGES) & 1);
+                const double* As = smem + s * SS;
+                const double* Bs = As + SA;
+                double a[2][FM], b[2][FN];
+                auto load_frags = [&](int buf, int k) {
+#pragma unroll
+                    for (int mi = 0; mi < FM; ++mi)
+                        a[buf][mi] = frag_ld<AK, Cfg::BM, BK>(As, k, wm + mi * 8 + g4);
+#pragma unroll
+                    for (int ni = 0; ni < FN; ++ni)
+                        b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g4);
+                };
+                const int nks = kt + 1 < kts ? BK / 4 : (kvl + 3) / 4;
+                load_frags(0, t);
+#pragma unroll
+                for (int ks = 0; ks < BK / 4; ++ks) {
+                    if (ks < nks) {
+                        const int cur = ks & 1;
+                        if (ks + 1 < BK / 4) load_frags(cur ^ 1, (ks + 1) * 4 + t);
+#pragma unroll
+                        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                            for (int ni = 0; ni < FN; ++ni)
+                                dmma884(acc.c[mi][ni], a[cur][mi], b[cur][ni]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);
+            }
+            epi(it, acc);
+        }
+    }
+};
+
 // Visit every accumulator element: f(m_local, n_local, v(n), v(n+1)).
 template <class Cfg, class F>
 __device__ __forceinline__ void acc_foreach_pair(const Acc<Cfg>& acc, F&& f) {

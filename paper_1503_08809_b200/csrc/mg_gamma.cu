@@ -19,6 +19,8 @@
 // is owned by exactly one CTA per launch and rows are reduced in a fixed order, so a run is
 // bitwise reproducible.
 #include <algorithm>
+#include <memory>
+#include <mutex>
 #include <type_traits>
 #include <cmath>
 #include <cstring>
@@ -89,7 +91,6 @@ constexpr int PAIR_BK = 32, PAIR_ST = 3;
 using Cfg128 = TileCfg<2, 4, 8, 4>;   // 128 x 128, 8 warps, 64 accumulators per lane
 using CfgX120 = TileCfg<5, 3, 3, 5>;  // 120 x 120, 15 warps, 30 accumulators per lane
 using CfgRun = CfgX120;                // run contraction: 15 consumer warps + 1 producer
-using RunPipe = PipeTMA<CfgRun, RUN_BK, RUN_ST, true, true>;
 using PairPipe = Pipe<Cfg128, PAIR_BK, PAIR_ST, ASrc::KMajor, true, 0>;
 constexpr int RUN_TM = CfgRun::BM;     // (row, c) slots per run tile = A panel width
 static_assert(RUN_TN == CfgRun::BN && RUN_LDB == ld_kmajor(RUN_TM) &&
@@ -152,60 +153,78 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
 //   slot = (row, c) flattened over the batch; WQT rows are p*Nxw wide (x unpadded when Nx is
 //   even); H rows are [c'][NxP] (x padded to the x-contraction's BK, pads stay zero).
 // ------------------------------------------------------------------------------------------
-struct RunProd {
-    const double* panel;  // this tile's A panel, rows of RUN_LDB doubles
-    const double* wqb;    // WQB rows of this (parity class, column block), from row jlo
-    int n_valid, kv_last;
-    __device__ int kvalid_last() const { return kv_last; }
-    __device__ uint32_t stage_bytes(int) const {
+// Persistent run contraction: item it = tile * NB + column block; items are strided over the
+// CTAs (one per SM).  The producer warp streams the next item while consumers write H.
+struct RunItems {
+    const MgTile* tiles;
+    const int64_t* poff;
+    const double* panel;
+    const MgRow* rows;
+    const double* WQB;
+    longlong2 wbase;
+    int2 wrows;
+    int NB;
+    __device__ int ktiles(int it) const {
+        const MgTile& t = tiles[it / NB];
+        return (t.jhi - t.jlo + RUN_BK) / RUN_BK;
+    }
+    __device__ int kvalid_last(int it) const {
+        const MgTile& t = tiles[it / NB];
+        const int nk = t.jhi - t.jlo + 1;
+        return nk - (nk - 1) / RUN_BK * RUN_BK;
+    }
+    __device__ uint32_t stage_bytes(int, int) const {
         return 2 * RUN_BK * RUN_LDB * (uint32_t)sizeof(double);
     }
-    // two bulk copies: 32 panel rows and 32 WQB rows (zero rows pad every class's end)
-    __device__ void bulk_rows(int kt, double* As, double* Bs, int lane, uint64_t* bar) const {
-        if (lane == 0)
-            bulk_g2s(As, panel + (int64_t)kt * RUN_BK * RUN_LDB,
+    __device__ void bulk_rows(int it, int kt, double* As, double* Bs, int lane,
+                              uint64_t* bar) const {
+        if (lane > 1) return;
+        const int ti = it / NB, nb = it - ti * NB;
+        const MgTile& t = tiles[ti];
+        if (lane == 0) {
+            bulk_g2s(As, panel + poff[ti] + (int64_t)kt * RUN_BK * RUN_LDB,
                      RUN_BK * RUN_LDB * sizeof(double), bar);
-        else if (lane == 1)
-            bulk_g2s(Bs, wqb + (int64_t)kt * RUN_BK * RUN_LDB,
-                     RUN_BK * RUN_LDB * sizeof(double), bar);
+        } else {
+            const int par = rows[t.row0].par;
+            const double* w = WQB + (par ? wbase.y : wbase.x) +
+                              ((int64_t)nb * (par ? wrows.y : wrows.x) + t.jlo + kt * RUN_BK) *
+                                  RUN_LDB;
+            bulk_g2s(Bs, w, RUN_BK * RUN_LDB * sizeof(double), bar);
+        }
     }
 };
+using RunPipeP = PipeTMAPersistent<CfgRun, RUN_BK, RUN_ST, true, true>;
 
-__global__ void __launch_bounds__(RunPipe::THREADS, 1)
-k_run_contract(const MgTile* __restrict__ tiles, const int64_t* __restrict__ poff,
+__global__ void __launch_bounds__(RunPipeP::THREADS, 1)
+k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __restrict__ poff,
                const double* __restrict__ panel, int row_base, const MgRow* __restrict__ rows,
                const double* __restrict__ WQB, int p, int Nx, int Nxw, int NxP,
                longlong2 wbase, int2 wrows, double* __restrict__ H) {
     extern __shared__ __align__(16) double smem[];
-    const MgTile tl = tiles[blockIdx.y];
-    const int n0 = blockIdx.x * CfgRun::BN;
     const int64_t ldb = (int64_t)p * Nxw;
-    const int par = rows[tl.row0].par;
-    const int nk = tl.jhi - tl.jlo + 1;
-    RunProd pr;
-    pr.panel = panel + poff[blockIdx.y];
-    pr.wqb = WQB + (par ? wbase.y : wbase.x) +
-             ((int64_t)blockIdx.x * (par ? wrows.y : wrows.x) + tl.jlo) * RUN_LDB;
-    pr.n_valid = (int)(ldb - n0 < CfgRun::BN ? ldb - n0 : CfgRun::BN);
-    pr.kv_last = nk - (nk - 1) / RUN_BK * RUN_BK;
-    Acc<CfgRun> acc;
-    if (!RunPipe::run((nk + RUN_BK - 1) / RUN_BK, pr, smem, acc)) return;  // producer warp
-    const int64_t hbase = (int64_t)(tl.row0 - row_base) * p + tl.c0;  // H row of slot 0
-    acc_foreach_pair<CfgRun>(acc, [&](int m, int n, double v0, double v1) {
-        const int gn = n0 + n;
-        if (m < tl.nslots && gn < ldb) {
-            const int cp = gn / Nxw, x = gn - cp * Nxw;   // Nxw even: (gn, gn+1) share c'
-            const int64_t slot = hbase + m, rr = slot / p;
-            const int c = (int)(slot - rr * p);
-            double* h = H + ((rr * (NxP / X_BK) + x / X_BK) * (p * p) + c * p + cp) * X_LDK +
-                        (x & (X_BK - 1));
-            if (x + 1 < Nx) {
-                *reinterpret_cast<double2*>(h) = make_double2(v0, v1);
-            } else if (x < Nx) {
-                h[0] = v0;
+    RunItems items{tiles, poff, panel, rows, WQB, wbase, wrows, (int)((ldb + RUN_TN - 1) / RUN_TN)};
+    const int nitems = ntiles * items.NB;
+    RunPipeP::run(blockIdx.x, gridDim.x, nitems, items, [&](int it, const Acc<CfgRun>& acc) {
+        const int ti = it / items.NB, nb = it - ti * items.NB;
+        const MgTile tl = tiles[ti];
+        const int n0 = nb * RUN_TN;
+        const int64_t hbase = (int64_t)(tl.row0 - row_base) * p + tl.c0;  // H row of slot 0
+        acc_foreach_pair<CfgRun>(acc, [&](int m, int n, double v0, double v1) {
+            const int gn = n0 + n;
+            if (m < tl.nslots && gn < ldb) {
+                const int cp = gn / Nxw, x = gn - cp * Nxw;  // Nxw even: (gn, gn+1) share c'
+                const int64_t slot = hbase + m, rr = slot / p;
+                const int c = (int)(slot - rr * p);
+                double* h = H + ((rr * (NxP / X_BK) + x / X_BK) * (p * p) + c * p + cp) * X_LDK +
+                            (x & (X_BK - 1));
+                if (x + 1 < Nx) {
+                    *reinterpret_cast<double2*>(h) = make_double2(v0, v1);
+                } else if (x < Nx) {
+                    h[0] = v0;
+                }
             }
-        }
-    });
+        });
+    }, smem);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -326,6 +345,68 @@ k_x_contract(const double* __restrict__ S, const double* __restrict__ H, int row
             if (cc + 1 < pp) Gr[(int64_t)(cc + 1) * P2 + prr] = v1;
         }
     });
+}
+
+// Persistent x contraction for the 120 x 120 tile: item it = (row r, M tile, N tile).
+struct XItems {
+    const double* S;
+    const double* H;
+    int P2, pp, XB, MT, NT;
+    __device__ void decode(int it, int& r, int& mt, int& nt) const {
+        nt = it % NT;
+        mt = (it / NT) % MT;
+        r = it / (NT * MT);
+    }
+    __device__ int ktiles(int) const { return XB; }
+    int kv_last;
+    __device__ int kvalid_last(int) const { return kv_last; }
+    __device__ uint32_t stage_bytes(int it, int) const {
+        int r, mt, nt;
+        decode(it, r, mt, nt);
+        const int mv = min(CfgX120::BM, P2 - mt * CfgX120::BM);
+        const int nv = min(CfgX120::BN, pp - nt * CfgX120::BN);
+        return (mv + nv) * X_LDK * (uint32_t)sizeof(double);
+    }
+    __device__ void bulk_rows(int it, int kt, double* As, double* Bs, int lane,
+                              uint64_t* bar) const {
+        if (lane > 1) return;
+        int r, mt, nt;
+        decode(it, r, mt, nt);
+        if (lane == 0) {
+            const int mv = min(CfgX120::BM, P2 - mt * CfgX120::BM);
+            bulk_g2s(As, S + (((int64_t)r * XB + kt) * P2 + mt * CfgX120::BM) * X_LDK,
+                     mv * X_LDK * sizeof(double), bar);
+        } else {
+            const int nv = min(CfgX120::BN, pp - nt * CfgX120::BN);
+            bulk_g2s(Bs, H + (((int64_t)r * XB + kt) * pp + nt * CfgX120::BN) * X_LDK,
+                     nv * X_LDK * sizeof(double), bar);
+        }
+    }
+};
+using XPipeP = PipeTMAPersistent<CfgX120, X_BK, 3, false, false>;
+
+__global__ void __launch_bounds__(XPipeP::THREADS, 1)
+k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int nrows,
+               int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* __restrict__ G) {
+    extern __shared__ __align__(16) double smem[];
+    const int pp = p * p;
+    XItems items{S, H, P2, pp, NxP / X_BK, (P2 + CfgX120::BM - 1) / CfgX120::BM,
+                 (pp + CfgX120::BN - 1) / CfgX120::BN, 0};
+    items.kv_last = Nx - (items.XB - 1) * X_BK;
+    const int nitems = nrows * items.MT * items.NT;
+    XPipeP::run(blockIdx.x, gridDim.x, nitems, items, [&](int it, const Acc<CfgX120>& acc) {
+        int r, mt, nt;
+        items.decode(it, r, mt, nt);
+        const int m0 = mt * CfgX120::BM, n0 = nt * CfgX120::BN;
+        double* Gr = G + (int64_t)(row_b1 + r - row_b3) * pp * P2;
+        acc_foreach_pair<CfgX120>(acc, [&](int m, int n, double v0, double v1) {
+            const int prr = m0 + m, cc = n0 + n;
+            if (prr < P2) {
+                if (cc < pp) Gr[(int64_t)cc * P2 + prr] = v0;
+                if (cc + 1 < pp) Gr[(int64_t)(cc + 1) * P2 + prr] = v1;
+            }
+        });
+    }, smem);
 }
 
 // Tile choice for the x contraction: the config with the least padded M x N area.
@@ -476,6 +557,7 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
         MG_REQUIRE(0 <= a && a <= b && b <= c && c < p, "mapping triples must satisfy i<=j<=k<p");
         md[3 * i] = (int)a; md[3 * i + 1] = (int)b; md[3 * i + 2] = (int)c;
     }
+    P->sc = scratch_pool(P->device);
     P->p = p; P->Nx = Nx; P->nm = n; P->l_min = l_min; P->l_max = l_max; P->L = L;
     P->h2_mode = h2_mode;
     P->NxP = (int)round_up(Nx, X_BK);
@@ -553,6 +635,15 @@ void build_rows(const mg_plan* P, int l2a, int l2b, const int* s, const int* e,
             }
         }
     }
+}
+
+MgScratch* scratch_pool(int device) {
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<MgScratch>> pools;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)pools.size() <= device) pools.resize(device + 1);
+    if (!pools[device]) pools[device].reset(new MgScratch());
+    return pools[device].get();
 }
 
 // Batch geometry: K1/K2 work on nb1 rows at a time (H buffer), K3 on nb3 (G buffer).
@@ -653,27 +744,27 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     }
     tile_first.push_back((int)tiles.size());
 
-    P->rows.upload(hrows.data(), hrows.size(), st);
-    P->zoff.upload(hzoff.data(), hzoff.size(), st);
-    P->tiles.upload(tiles.data(), tiles.size(), st);
-    P->poff.upload(poff.data(), poff.size(), st);
+    P->sc->rows.upload(hrows.data(), hrows.size(), st);
+    P->sc->zoff.upload(hzoff.data(), hzoff.size(), st);
+    P->sc->tiles.upload(tiles.data(), tiles.size(), st);
+    P->sc->poff.upload(poff.data(), poff.size(), st);
     int64_t maxzt = 1, maxpanel = 1;
     for (size_t bi = 0; bi + 1 < tile_first.size(); ++bi) {
         int64_t b1 = bi * (int64_t)nb1, e1 = std::min<int64_t>(b1 + nb1, nrows);
         maxzt = std::max(maxzt, hzoff[e1] - hzoff[b1]);
         maxpanel = std::max(maxpanel, panel_len[bi]);
     }
-    if (dt1) P->ZT.ensure(maxzt);
-    P->panel.ensure(maxpanel);
+    if (dt1) P->sc->ZT.ensure(maxzt);
+    P->sc->panel.ensure(maxpanel);
     const size_t hsize = (size_t)nb1 * pp * (NxP / X_BK) * X_LDK;
-    if (P->H.n < hsize) {  // x pads of H are never written: zero them once
-        P->H.ensure(hsize);
-        MG_CUDA(cudaMemsetAsync(P->H.p, 0, P->H.n * sizeof(double), st));
+    if (P->sc->H.n < hsize) {  // x pads of H are never written: zero them once
+        P->sc->H.ensure(hsize);
+        MG_CUDA(cudaMemsetAsync(P->sc->H.p, 0, P->sc->H.n * sizeof(double), st));
     }
-    P->G.ensure((size_t)nb3 * pp * P2);
-    P->S.ensure((size_t)nb1 * P2 * (NxP / X_BK) * X_LDK);
-    P->R.ensure((size_t)nb3 * ldr);
-    P->Sq.ensure((size_t)nb3 * ldq);
+    P->sc->G.ensure((size_t)nb3 * pp * P2);
+    P->sc->S.ensure((size_t)nb1 * P2 * (NxP / X_BK) * X_LDK);
+    P->sc->R.ensure((size_t)nb3 * ldr);
+    P->sc->Sq.ensure((size_t)nb3 * ldq);
     // K-split of the pair contraction so that its grid fills the 148 SMs
     const int tiles3 = ceil_div(ncols, Cfg128::BN) * ceil_div(P2, Cfg128::BM);
     int nsplit = 1;
@@ -687,12 +778,12 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         }
     }
     const int64_t zsplit = (int64_t)P2 * ncols;
-    P->Z.ensure((size_t)nsplit * zsplit);
-    MG_CUDA(cudaMemsetAsync(P->Z.p, 0, (size_t)nsplit * zsplit * sizeof(double), st));
+    P->sc->Z.ensure((size_t)nsplit * zsplit);
+    MG_CUDA(cudaMemsetAsync(P->sc->Z.p, 0, (size_t)nsplit * zsplit * sizeof(double), st));
     P->gamma.ensure((size_t)nm * nm);
 
     static bool attr_done = false;
-    const size_t smem_run = RunPipe::smem_bytes;
+    const size_t smem_run = RunPipeP::smem_bytes;
     const XTile xt = choose_xtile(P2, pp);
     const size_t smem_x = xt == XTile::T120 ? XPipeT<CfgX120>::smem_bytes
                                             : XPipeT<Cfg128>::smem_bytes;
@@ -700,9 +791,8 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     if (!attr_done) {
         MG_CUDA(cudaFuncSetAttribute(k_run_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_run));
-        MG_CUDA(cudaFuncSetAttribute(k_x_contract<CfgX120>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)XPipeT<CfgX120>::smem_bytes));
+        MG_CUDA(cudaFuncSetAttribute(k_x_contract_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)XPipeP::smem_bytes));
         MG_CUDA(cudaFuncSetAttribute(k_x_contract<Cfg128>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)XPipeT<Cfg128>::smem_bytes));
@@ -712,6 +802,8 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     }
     DBuf<int> l0d;
     l0d.upload(P->l0, 2, st);
+    int num_sms = 148;
+    MG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, P->device));
 
     double f_run = 0, f_x = 0, f_pair = 0;
     int64_t launches = 0;
@@ -725,46 +817,42 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             const double* zt = nullptr;
             if (dt1) {
                 int64_t t0 = (*tri_of_row)[b1], t1 = (*tri_of_row)[e1];
-                MG_CUDA(cudaMemsetAsync(P->ZT.p, 0, (hzoff[e1] - zbase) * sizeof(double), st));
+                MG_CUDA(cudaMemsetAsync(P->sc->ZT.p, 0, (hzoff[e1] - zbase) * sizeof(double), st));
                 if (t1 > t0)
                     k_scatter_weights<<<std::min<int64_t>((t1 - t0 + 255) / 256, 4096), 256, 0,
                                         st>>>(dt1 + t0, dt2 + t0, dt3 + t0, dpos + t0, ddup + t0,
                                               t1 - t0, zbase, P->l_min, P->C.p, P->v.p,
-                                              P->lf.p, P->h2_mode, P->ZT.p);
+                                              P->lf.p, P->h2_mode, P->sc->ZT.p);
                 MG_LAUNCHED();
-                zt = P->ZT.p;
+                zt = P->sc->ZT.p;
             }
             int tf = tile_first[bidx], tl = tile_first[bidx + 1];
             prof_mark(P, 0, st);
             k_run_panels<<<tl - tf, PANEL_THREADS, max_tile_rows * PANEL_JC * sizeof(double),
-                           st>>>(P->tiles.p + tf, P->rows.p, P->poff.p + tf, P->zoff.p, zbase, zt,
+                           st>>>(P->sc->tiles.p + tf, P->sc->rows.p, P->sc->poff.p + tf, P->sc->zoff.p, zbase, zt,
                                  l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p,
-                                 P->h2_mode, P->panel.p);
+                                 P->h2_mode, P->sc->panel.p);
             MG_LAUNCHED();
             {
                 dim3 gs(ceil_div(P2, PP_CHUNK), nb);
-                k_pair_products<<<gs, 256, 0, st>>>(P->rows.p, (int)b1, P->QT.p, p, P2, NxP,
-                                                    P->l_min, P->S.p);
+                k_pair_products<<<gs, 256, 0, st>>>(P->sc->rows.p, (int)b1, P->QT.p, p, P2, NxP,
+                                                    P->l_min, P->sc->S.p);
                 MG_LAUNCHED();
             }
-            dim3 g1(ceil_div((int64_t)p * P->Nxw, CfgRun::BN), tl - tf);
             prof_mark(P, 1, st);
-            k_run_contract<<<g1, RunPipe::THREADS, smem_run, st>>>(P->tiles.p + tf, P->poff.p + tf,
-                                                             P->panel.p, (int)b1, P->rows.p,
-                                                             P->WQT.p, p, P->Nx, P->Nxw, NxP,
-                                                             make_longlong2(P->wbase[0], P->wbase[1]),
-                                                             make_int2(P->wrows[0], P->wrows[1]),
-                                                             P->H.p);
+            k_run_contract<<<num_sms, RunPipeP::THREADS, smem_run, st>>>(
+                P->sc->tiles.p + tf, tl - tf, P->sc->poff.p + tf, P->sc->panel.p, (int)b1, P->sc->rows.p,
+                P->WQT.p, p, P->Nx, P->Nxw, NxP, make_longlong2(P->wbase[0], P->wbase[1]),
+                make_int2(P->wrows[0], P->wrows[1]), P->sc->H.p);
             MG_LAUNCHED();
             prof_mark(P, 2, st);
             if (xt == XTile::T120) {
-                dim3 g2(ceil_div(pp, CfgX120::BN), ceil_div(P2, CfgX120::BM), nb);
-                k_x_contract<CfgX120><<<g2, XPipeT<CfgX120>::THREADS, smem_x, st>>>(
-                    P->S.p, P->H.p, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->G.p);
+                k_x_contract_p<<<num_sms, XPipeP::THREADS, XPipeP::smem_bytes, st>>>(
+                    P->sc->S.p, P->sc->H.p, nb, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
             } else {
                 dim3 g2(ceil_div(pp, Cfg128::BN), ceil_div(P2, Cfg128::BM), nb);
                 k_x_contract<Cfg128><<<g2, XPipeT<Cfg128>::THREADS, smem_x, st>>>(
-                    P->S.p, P->H.p, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->G.p);
+                    P->sc->S.p, P->sc->H.p, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
             }
             MG_LAUNCHED();
             launches += 4 + (dt1 ? 1 : 0);
@@ -777,21 +865,21 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         const int n3 = (int)(e3 - b3);
         prof_mark(P, 3, st);
         dim3 gg(std::min(ceil_div(ncols, 256), 64), n3);
-        k_gather<<<gg, 256, 0, st>>>(P->rows.p + b3, P->G.p, P->modes.p, P->q.p, P->L, P->l_min,
-                                     p, P2, nm, ldr, ldq, P->R.p, P->Sq.p);
+        k_gather<<<gg, 256, 0, st>>>(P->sc->rows.p + b3, P->sc->G.p, P->modes.p, P->q.p, P->L, P->l_min,
+                                     p, P2, nm, ldr, ldq, P->sc->R.p, P->sc->Sq.p);
         MG_LAUNCHED();
         const int per = (int)round_up(ceil_div(n3, nsplit), PAIR_BK);
         dim3 g3(ceil_div(ncols, Cfg128::BN), ceil_div(P2, Cfg128::BM), ceil_div(n3, per));
         prof_mark(P, 4, st);
-        k_pair_contract<<<g3, 256, smem_pair, st>>>(P->Sq.p, ldq, P->R.p, ldr, n3, per,
-                                                           P2, ncols, zsplit, P->Z.p);
+        k_pair_contract<<<g3, 256, smem_pair, st>>>(P->sc->Sq.p, ldq, P->sc->R.p, ldr, n3, per,
+                                                           P2, ncols, zsplit, P->sc->Z.p);
         MG_LAUNCHED();
         launches += 2;
         f_pair += 2.0 * P2 * ncols * (double)n3;
     }
     prof_mark(P, 5, st);
     k_final<<<std::min<int64_t>(((int64_t)nm * nm + 255) / 256, 4096), 256, 0, st>>>(
-        P->Z.p, nsplit, zsplit, P->modes.p, p, nm, P->gamma.p);
+        P->sc->Z.p, nsplit, zsplit, P->modes.p, p, nm, P->gamma.p);
     MG_LAUNCHED();
     prof_mark(P, -1, st);
     launches += 1;

@@ -22,6 +22,18 @@ struct MgTile {
 
 constexpr int MG_NPROF = 6;
 
+// Batch scratch, pooled per device so that one-shot calls (the drop-in API) do not pay for
+// allocating and zeroing gigabytes every time.  Buffers only grow; they are zeroed when
+// (re)allocated (H's x pads must never hold NaN) and never shrink.  Plans on one device are
+// not re-entrant (documented in include/modal_b200.h), so sharing is safe.
+struct MgScratch {
+    mg::DBuf<double> ZT, panel, H, S, G, R, Sq, Z;
+    mg::DBuf<int64_t> poff;
+    mg::DBuf<MgRow> rows;
+    mg::DBuf<int64_t> zoff;
+    mg::DBuf<MgTile> tiles;
+};
+
 struct mg_plan {
     int device = 0;
     int p = 0, Nx = 0, NxP = 0, nm = 0, l_min = 2, l_max = 2, L = 0, h2_mode = 0;
@@ -34,11 +46,8 @@ struct mg_plan {
     mg::DBuf<double> q, QT, WQT, C, v, lf, wr2;
     mg::DBuf<int> modes;  // [nm][3]
     // scratch
-    mg::DBuf<double> ZT, panel, H, S, G, R, Sq, Z, gamma;
-    mg::DBuf<int64_t> poff;
-    mg::DBuf<MgRow> rows;
-    mg::DBuf<int64_t> zoff;
-    mg::DBuf<MgTile> tiles;
+    mg::DBuf<double> gamma;     // Γ of the last execute (owned by the plan)
+    MgScratch* sc = nullptr;    // per-device scratch pool (shared by plans on the device)
     int nb1 = 0, nb3 = 0;  // rows per run/x-contraction batch, rows per pair-contraction batch
     // stats of the last execute
     double flops_run = 0, flops_x = 0, flops_pair = 0;
@@ -57,6 +66,7 @@ struct mg_plan {
 };
 
 namespace mg {
+MgScratch* scratch_pool(int device);
 void plan_init(mg_plan* P, const double* q, const double* qt_host, const double* qt_dev,
                const double* C, const double* v, const double* wr2, const int64_t* modes,
                int p, int Nx, int n, int l_min, int l_max, int h2_mode);
