@@ -19,6 +19,8 @@ Differences that do not change results:
 
 from __future__ import annotations
 
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from . import _native as nat
@@ -29,6 +31,7 @@ __all__ = ["gamma3d_matrix", "DomainRange", "DEFAULT_BLOCK", "domain_count",
            "domain_triples", "triple_weights"]
 
 DEFAULT_BLOCK = 64
+_FP_POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="mg-fingerprint")
 
 
 class DomainRange:
@@ -103,6 +106,11 @@ def triple_weights(C, v, l_min: int, l_max: int, begin: int = 0, end: int | None
 
 def _base_meta(tables, grid, mapping, integrator, h2_mode, block, workers):
     """Provenance keys of engine3d.py:139-153,172-174."""
+    return _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers,
+                      tables.fingerprint(), grid.fingerprint(), mapping.fingerprint())
+
+
+def _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers, ft, fg, fm):
     return {
         "engine": "modal3d",
         "l_min": tables.l_min,
@@ -110,9 +118,9 @@ def _base_meta(tables, grid, mapping, integrator, h2_mode, block, workers):
         "p_max": tables.p_max,
         "n_max": mapping.n_max,
         "integrator": integrator,
-        "tables": tables.fingerprint(),
-        "grid": grid.fingerprint(),
-        "mapping": mapping.fingerprint(),
+        "tables": ft,
+        "grid": fg,
+        "mapping": fm,
         "h2_mode": h2_mode,
         "block": block,
         "workers": workers,
@@ -166,7 +174,15 @@ def gamma3d_matrix(tables, mapping, grid, h2_mode: str = "gosper", integrator: s
     wr2 = np.ascontiguousarray(x_weights(grid.r, integrator), np.float64)
     p, nx, n = q.shape[0], qt.shape[1], entries.shape[0]
     l_min, l_max = int(tables.l_min), int(tables.l_max)
-    meta = _base_meta(tables, grid, mapping, integrator, h2_mode, block, workers)
+    # The sha256 fingerprints of the inputs (meta, engine3d.py:139-153) cost ~0.25 s for a
+    # config-1 q̃; hashlib and the ctypes call both release the GIL, so they overlap.
+    fp = _FP_POOL.submit(lambda: (tables.fingerprint(), grid.fingerprint(),
+                                  mapping.fingerprint()))
+
+    def meta():
+        return _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers,
+                          *fp.result())
+
     out = np.zeros((n, n))
     lib = nat.lib()
     common = (nat.ptr(q), nat.ptr(qt), nat.ptr(C), nat.ptr(v), nat.ptr(wr2), nat.ptr(entries),
@@ -180,11 +196,11 @@ def gamma3d_matrix(tables, mapping, grid, h2_mode: str = "gosper", integrator: s
         if rng is None:
             nat.check(lib.mg_gamma_sep_triples(*common, nat.ptr(l1), nat.ptr(l2), nat.ptr(l3),
                                                int(l1.size), int(device), nat.ptr(out)))
-            return GammaMatrix(out, meta)
+            return GammaMatrix(out, meta())
     begin, end = rng
     if end > begin:
         nat.check(lib.mg_gamma_sep(*common, int(begin), int(end), int(device), nat.ptr(out)))
-    return GammaMatrix(out, meta)
+    return GammaMatrix(out, meta())
 
 
 def _detect_contiguous(l1, l2, l3, l_min, l_max):
