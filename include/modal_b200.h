@@ -174,6 +174,22 @@ int mg_gamma_nonsep(const double* q, const double* qt, const double* C, const do
                     const int32_t* l2, const int32_t* l3, const double* W, int64_t count,
                     int device, double* b);
 
+/* ---------------------------------------------------------------------------------------
+ * μ-quadrature ("separable", Modal2D) engine: replaces build_ptable / gamma2d_matrix
+ * (engine2d.py:62-95, 187-211).
+ *   lw [L] = (2l+1)/(v_l sqrt C_l); legendre [L][nmu] = P_l(μ_m) for l = l_min..l_max
+ *   ptable [p][p][Nx][nmu] = Σ_l lw_l q_a(l) q̃_b(x,l) P_l(μ_m) (ascending-l Kahan, the
+ *   reference's operation order: bit-identical table)
+ *   gamma [n][n] = Σ_x wr2_x Σ_m mu_w[m] perm3(P[rows(n),cols(n')](x,m)) / (48π)
+ * mg_gamma2d takes either a precomputed ptable or (q, qt, lw, legendre) to build it.
+ * ------------------------------------------------------------------------------------- */
+int mg_ptable(const double* q, const double* qt, const double* lw, const double* legendre,
+              int p, int Nx, int L, int nmu, int device, double* ptable);
+int mg_gamma2d(const double* q, const double* qt, const double* lw, const double* legendre,
+               const double* ptable, const double* mu_w, const double* wr2,
+               const int64_t* modes, int p, int Nx, int L, int nmu, int n, int device,
+               double* gamma);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,6 +52,8 @@ _SIGS = {
     "mg_build_qtilde_dev": (_i, [_vp, _vp, _i, _vp, _i, _vp, _vp, _i, _i, _i, _d, _d, _d, _i,
                                  _vp, _vp, _vp]),
     "mg_bessel_table": (_i, [_vp, _i, _i, _i, _vp]),
+    "mg_ptable": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp]),
+    "mg_gamma2d": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp]),
     "mg_gamma_nonsep": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp,
                              _vp, _vp, _i64, _i, _vp]),
 }

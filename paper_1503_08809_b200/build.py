@@ -16,7 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_native", "libmodal_b200.so")
-SOURCES = ["mg_api.cu", "mg_gamma.cu", "mg_qtilde.cu"]
+SOURCES = ["mg_api.cu", "mg_gamma.cu", "mg_qtilde.cu", "mg_gamma2d.cu"]
 HEADERS = ["mg_common.cuh", "mg_domain.cuh", "mg_dmma.cuh", "mg_gamma.cuh", "mg_bessel.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -19,6 +19,10 @@ void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x
                       double X, double kd, double amp, double* C_dev, double* qt_dev,
                       double* delta_out_dev, cudaStream_t s);
 void bessel_table(const double* z, int nz, int l_max, double* out);
+void ptable_dev(const double* q, const double* qt, const double* lw, const double* leg, int p,
+                int Nx, int L, int nmu, double* P_dev);
+void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int Nx, int nmu,
+                 const double* mu_w, const double* wr2, double* gamma_host);
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -343,6 +347,44 @@ int mg_bessel_table(const double* z, int nz, int l_max, int device, double* out)
         MG_REQUIRE(z && out, "null argument");
         DeviceGuard g(device);
         bessel_table(z, nz, l_max, out);
+    });
+}
+
+int mg_ptable(const double* q, const double* qt, const double* lw, const double* legendre,
+              int p, int Nx, int L, int nmu, int device, double* ptable) {
+    return guarded([&] {
+        MG_REQUIRE(q && qt && lw && legendre && ptable, "null argument");
+        MG_REQUIRE(p >= 1 && Nx >= 1 && L >= 1 && nmu >= 1, "invalid sizes");
+        DeviceGuard g(device);
+        const size_t np = (size_t)p * p * Nx * nmu;
+        DBuf<double> dP(np);
+        ptable_dev(q, qt, lw, legendre, p, Nx, L, nmu, dP.p);
+        MG_CUDA(cudaMemcpy(ptable, dP.p, np * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+int mg_gamma2d(const double* q, const double* qt, const double* lw, const double* legendre,
+               const double* ptable, const double* mu_w, const double* wr2,
+               const int64_t* modes, int p, int Nx, int L, int nmu, int n, int device,
+               double* gamma) {
+    return guarded([&] {
+        MG_REQUIRE(mu_w && wr2 && modes && gamma, "null argument");
+        MG_REQUIRE(ptable || (q && qt && lw && legendre), "need the P table or its inputs");
+        MG_REQUIRE(p >= 1 && Nx >= 1 && nmu >= 1 && n >= 1, "invalid sizes");
+        std::vector<int> md(3 * (size_t)n);
+        for (int i = 0; i < n; ++i) {
+            int64_t a = modes[3 * i], b = modes[3 * i + 1], c = modes[3 * i + 2];
+            MG_REQUIRE(0 <= a && a <= b && b <= c && c < p, "mapping triples must satisfy i<=j<=k<p");
+            md[3 * i] = (int)a; md[3 * i + 1] = (int)b; md[3 * i + 2] = (int)c;
+        }
+        DeviceGuard g(device);
+        const size_t np = (size_t)p * p * Nx * nmu;
+        DBuf<double> dP(np);
+        if (ptable)
+            dP.upload(ptable, np);
+        else
+            ptable_dev(q, qt, lw, legendre, p, Nx, L, nmu, dP.p);
+        gamma2d_dev(dP.p, md.data(), n, p, Nx, nmu, mu_w, wr2, gamma);
     });
 }
 

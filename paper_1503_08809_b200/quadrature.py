@@ -100,3 +100,75 @@ def x_weights(r, method: str = "trap") -> np.ndarray:
     """wr2 = integration_weights(r, method) * r**2 (engine3d.py:126)."""
     r = np.asarray(r, dtype=np.float64)
     return integration_weights(r, method) * r ** 2
+
+
+# ------------------------------------------------------------------------------------------
+# Gauss-Legendre rule and Legendre table for the 2D (mu-quadrature) engine
+# (quadrature.py:38-112 of the reference; restated with the same Newton scheme so the nodes
+#  and weights agree with the reference to the last bit or so)
+# ------------------------------------------------------------------------------------------
+
+class QuadratureRule:
+    """Gauss-Legendre nodes and weights on [-1, 1]."""
+
+    def __init__(self, nodes, weights):
+        self.nodes = np.asarray(nodes, dtype=np.float64)
+        self.weights = np.asarray(weights, dtype=np.float64)
+
+    @property
+    def n(self) -> int:
+        return int(self.nodes.size)
+
+
+def _legendre_pd(n: int, x: np.ndarray):
+    p0, p1 = np.ones_like(x), x.copy()
+    if n == 0:
+        return p0, np.zeros_like(x)
+    for k in range(1, n):
+        p0, p1 = p1, ((2 * k + 1) * x * p1 - k * p0) / (k + 1)
+    return p1, n * (x * p1 - p0) / (x * x - 1.0)
+
+
+def gauss_legendre(n: int) -> QuadratureRule:
+    """n-node rule: Newton on P_n from Chebyshev-angle guesses, one clean-up step, exact
+    symmetry enforced (reference quadrature.py:68-98)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if n == 1:
+        return QuadratureRule(np.zeros(1), np.full(1, 2.0))
+    b = np.arange(n, dtype=np.float64)
+    x = np.cos(np.pi * (4 * b + 3) / (4 * n + 2))
+    for _ in range(100):
+        p, dp = _legendre_pd(n, x)
+        dx = p / dp
+        x = x - dx
+        if np.max(np.abs(dx)) < 1e-15:
+            p, dp = _legendre_pd(n, x)
+            x = x - p / dp
+            break
+    else:
+        raise RuntimeError(f"Gauss-Legendre Newton iteration failed at n={n}")
+    x = np.sort(x)
+    x = 0.5 * (x - x[::-1])
+    _, dp = _legendre_pd(n, x)
+    w = 2.0 / ((1.0 - x * x) * dp * dp)
+    return QuadratureRule(x, 0.5 * (w + w[::-1]))
+
+
+def legendre_table(l_max: int, rule) -> np.ndarray:
+    """P_l at every node, [l_max+1, n], upward recurrence (reference quadrature.py:101-112)."""
+    if l_max < 0:
+        raise ValueError("l_max must be >= 0")
+    x = np.asarray(rule.nodes, dtype=np.float64)
+    t = np.empty((l_max + 1, x.size))
+    t[0] = 1.0
+    if l_max >= 1:
+        t[1] = x
+    for l in range(1, l_max):
+        t[l + 1] = ((2 * l + 1) * x * t[l] - l * t[l - 1]) / (l + 1)
+    return t
+
+
+def default_mu_points(l_max: int) -> int:
+    """Exact for the degree-3 l_max integrand (reference engine2d.py:40-41)."""
+    return -(-(3 * l_max + 1) // 2) + 2

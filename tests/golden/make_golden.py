@@ -119,7 +119,37 @@ def c0_golden():
     return out
 
 
+def io_and_2d_golden():
+    """Reference Γ files (harness.serialize_gamma) and the 2D engine's Γ (engine2d)."""
+    from cmbproj import harness
+    out = {}
+    for tag, (lmin, lmax, p, nr, nmu) in {"desk": (2, 16, 3, 54, None),
+                                          "desk32": (2, 32, 4, 216, 50)}.items():
+        grid = cp.default_radial_grid(nr)
+        t = cp.synthesize_basis(p, lmin, lmax, grid)
+        m = cp.default_mode_mapping(p)
+        rule = cp.gauss_legendre(nmu or cp.default_mu_points(lmax))
+        leg = cp.legendre_table(lmax, rule)
+        out[f"{tag}_mu_nodes"], out[f"{tag}_mu_weights"] = rule.nodes, rule.weights
+        out[f"{tag}_gamma2d"] = cp.gamma2d_matrix(t, m, grid, rule, leg).values
+        out[f"{tag}_ptable"] = cp.build_ptable(t, grid, rule, leg).values
+        out[f"{tag}_gamma2d_naive_00"] = np.array(
+            cp.gamma2d_entry_naive(0, 0, t, m, grid, rule, leg))
+        out[f"{tag}_gamma3d_exact"] = cp.gamma3d_matrix(t, m, grid, h2_mode="exact").values
+        if tag == "desk":
+            g = cp.gamma3d_matrix(t, m, grid)
+            harness.serialize_gamma(g, os.path.join(HERE, "desk_gamma.csv"), "csv")
+            harness.serialize_gamma(g, os.path.join(HERE, "desk_gamma.bin"), "bin")
+    return out
+
+
 def main():
+    if "--only-io2d" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "io2d.npz"), **io_and_2d_golden())
+        print("io2d.npz")
+        return
+    np.savez_compressed(os.path.join(HERE, "io2d.npz"), **io_and_2d_golden())
+    print("io2d.npz")
     np.savez_compressed(os.path.join(HERE, "domain.npz"), **domain_golden())
     print("domain.npz")
     np.savez_compressed(os.path.join(HERE, "desk.npz"), **desk_golden())

@@ -240,3 +240,77 @@ def test_large_config_partials(cfg, ntri):
         want = ref.gamma3d(hi.q, qt, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max, a, a + ntri,
                            workers=8, block=8)
         assert frob_rel(got, want) < 1e-10
+
+
+class TestLateLate:
+    """⟨Q,Q⟩ = the Γ' engine with q̃ -> q, one x point, C -> v²."""
+
+    def oracle(self, t, m, h2_mode="gosper"):
+        qt = t.q[:, None, :]
+        return ref.gamma3d(t.q, qt, t.v * t.v, t.v, np.ones(1), m.entries, t.l_min, t.l_max,
+                           h2_mode=h2_mode)
+
+    @pytest.mark.parametrize("tag", ["desk", "desk32"])
+    def test_against_oracle(self, g_desk, tag):
+        from paper_1503_08809_b200 import gamma_late_late
+        t, m, r = desk_problem(g_desk, tag)
+        got = gamma_late_late(t, m).values
+        want = self.oracle(t, m)
+        assert frob_rel(got, want) < 1e-12
+        assert np.allclose(got, got.T, rtol=1e-12, atol=0)       # symmetric inner product
+
+    def test_c0_and_estimator(self, g_c0):
+        from paper_1503_08809_b200 import gamma_estimator
+        hi = host_inputs("c0")
+        t = BasisTables(hi.q, g_c0["qt"], g_c0["C"], hi.v, 2, 200)
+        m = ModeMapping(hi.entries, 6)
+        full, qq, gp = gamma_estimator(t, m, RadialGrid(hi.x))
+        assert frob_rel(qq.values, self.oracle(t, m)) < 1e-12
+        assert frob_rel(gp.values, g_c0["gamma"]) < 1e-10
+        assert frob_rel(qq.values @ full.values, g_c0["gamma"]) < 1e-9
+        assert np.all(np.linalg.eigvalsh(qq.values) > 0)           # positive definite
+
+
+class TestGamma2D:
+    """μ-quadrature engine vs the reference's engine2d (golden io2d.npz) and the
+    2D ≡ 3D-exact identity (acceptance criterion 1, test_acceptance.py:50-57)."""
+
+    def setup(self, g_desk, g2, tag, nmu):
+        from paper_1503_08809_b200 import gauss_legendre, legendre_table
+        t, m, r = desk_problem(g_desk, tag)
+        rule = gauss_legendre(nmu)
+        assert np.array_equal(rule.nodes, g2[f"{tag}_mu_nodes"])
+        return t, m, r, rule, legendre_table(t.l_max, rule)
+
+    @pytest.mark.parametrize("tag,nmu", [("desk", 27), ("desk32", 50)])
+    def test_ptable_bit_exact(self, g_desk, tag, nmu):
+        from conftest import golden
+        from paper_1503_08809_b200 import build_ptable
+        g2 = golden("io2d.npz")
+        t, m, r, rule, leg = self.setup(g_desk, g2, tag, nmu)
+        assert np.array_equal(build_ptable(t, r, rule, leg).values, g2[f"{tag}_ptable"])
+
+    @pytest.mark.parametrize("tag,nmu", [("desk", 27), ("desk32", 50)])
+    def test_gamma2d(self, g_desk, tag, nmu):
+        from conftest import golden
+        from paper_1503_08809_b200 import build_ptable, gamma2d_matrix
+        g2 = golden("io2d.npz")
+        t, m, r, rule, leg = self.setup(g_desk, g2, tag, nmu)
+        got = gamma2d_matrix(t, m, r, rule, leg)
+        assert gap_rel(got.values, g2[f"{tag}_gamma2d"]) < 1e-12
+        assert got.meta["engine"] == "modal2d" and got.meta["n_mu"] == nmu
+        pt = build_ptable(t, r, rule, leg)
+        again = gamma2d_matrix(t, m, r, rule, leg, ptable=pt).values
+        assert np.array_equal(again, got.values)
+        # criterion 1: separable (2D) == direct with exact weights (3D-exact)
+        g3 = gamma3d_matrix(t, m, r, h2_mode="exact").values
+        assert gap_rel(got.values, g3) < 1e-10
+
+    def test_budget_and_errors(self, g_desk):
+        from paper_1503_08809_b200 import build_ptable, gauss_legendre, legendre_table
+        t, m, r = desk_problem(g_desk, "desk")
+        rule = gauss_legendre(27)
+        with pytest.raises(MemoryError):
+            build_ptable(t, r, rule, legendre_table(16, rule), budget_bytes=1000)
+        with pytest.raises(ValueError):
+            build_ptable(t, r, rule, legendre_table(10, rule))
