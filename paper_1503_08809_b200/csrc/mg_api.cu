@@ -292,7 +292,9 @@ int mg_slab_plan(int l_min, int l_max, int p, int Nx, int nshards, int* bounds) 
                 int hi = (l2 & 1) == par ? l2 : l2 - 1;
                 if (lo > hi) continue;
                 double m = (hi - lo) / 2 + 1;
-                c += (double)p * p * Nx * m + pairs * p * p * Nx;
+                // calibrated model (scheduler.py slab_costs): run contraction pays ~20 padded
+                // l1 per row; per-row work is ~1.35x the x contraction
+                c += (double)p * p * Nx * (m + 20.0) + 1.35 * pairs * p * p * Nx;
             }
             cum[l2 - l_min + 1] = cum[l2 - l_min] + c;
         }

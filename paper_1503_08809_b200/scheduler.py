@@ -16,6 +16,9 @@ from .gamma import GammaMatrix
 
 __all__ = ["ChunkPlan", "make_plan", "merge_partials", "slab_costs", "slab_plan"]
 
+RUN_PAD = 20          # padded l1 values per row in the run contraction (measured)
+ROW_FACTOR = 1.35     # per-row work relative to the x contraction (measured)
+
 
 @dataclass(frozen=True)
 class ChunkPlan:
@@ -56,7 +59,10 @@ def slab_costs(l_min: int, l_max: int, p: int, n_x: int) -> np.ndarray:
     """Modelled FP64 work of every l2 value for the row-factorised Γ kernel.
 
     A (l2,l3)-row with an l1-run of m triples costs p^2·Nx·m FMAs (run contraction) plus
-    p(p+1)/2·p^2·Nx FMAs (x contraction) — see DESIGN.md §3.  Returns cost[l2 - l_min].
+    p(p+1)/2·p^2·Nx FMAs (x contraction) — see DESIGN.md §3.  Calibrated on a B200 (tools/
+    slab_balance.py): the run contraction pays ~20 padded l1 values per row (tile union and
+    k-tile rounding), and per-row work outside the two contractions (operand builds, gather,
+    pair contraction) adds ~35 % to the x contraction's cost.  Returns cost[l2 - l_min].
     """
     pairs = p * (p + 1) // 2
     out = np.zeros(l_max - l_min + 1)
@@ -67,7 +73,7 @@ def slab_costs(l_min: int, l_max: int, p: int, n_x: int) -> np.ndarray:
         hi = np.where((l3 & 1) == 0, l2, l2 - 1)        # l1 <= l2, l1+l2+l3 even
         m = np.maximum((hi - lo) // 2 + 1, 0)
         m = m[hi >= lo]
-        out[l2 - l_min] = p * p * n_x * m.sum() + m.size * pairs * p * p * n_x
+        out[l2 - l_min] = p * p * n_x * (m + RUN_PAD).sum() + m.size * ROW_FACTOR * pairs * p * p * n_x
     return out
 
 
