@@ -138,6 +138,24 @@ __device__ __forceinline__ double zm_exact(int l1, int l2, int l3, const double*
     return __dmul_rn(__ddiv_rn(h2, denom), (double)multiplicity(l1, l2, l3));
 }
 
+// Same quantity as zm_gosper, factored for the Γ pipeline (not bit-identical to NumPy, equal
+// to it within a few ulp): zm = mult/(72 π²) · f(l1) f(l2) f(l3) · g(L, L1, L2, L3),
+// f(l) = (2l+1)/(v_l sqrt C_l) (table fl[] indexed l - l_min),
+// g = (L+1/3) sqrt((L1+1/6)(L2+1/6)(L3+1/6)(L+1/6)) / ((L+1)(L1+1/3)(L2+1/3)(L3+1/3)(L+1/6)).
+__device__ __forceinline__ double zm_gosper_fast(int l1, int l2, int l3,
+                                                 const double* __restrict__ fl, int l_min) {
+    const double third = 1.0 / 3.0, sixth = 1.0 / 6.0;
+    const double inv72pi2 = 1.0 / (72.0 * 9.869604401089358);
+    const double L = (double)(l1 + l2 + l3);
+    const double La = (double)(l2 + l3 - l1), Lb = (double)(l1 + l3 - l2),
+                 Lc = (double)(l1 + l2 - l3);
+    const double s = (La + sixth) * (Lb + sixth) * (Lc + sixth) * (L + sixth);
+    const double den = (L + 1.0) * (La + third) * (Lb + third) * (Lc + third) * (L + sixth);
+    const double g = (L + third) * sqrt(s) / den;
+    return (double)multiplicity(l1, l2, l3) * inv72pi2 * fl[l1 - l_min] * fl[l2 - l_min] *
+           fl[l3 - l_min] * g;
+}
+
 __device__ __forceinline__ double zm_weight(int mode, int l1, int l2, int l3,
                                             const double* __restrict__ C,
                                             const double* __restrict__ v, int l_min,

@@ -106,7 +106,8 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
              const double* __restrict__ ZT, const int* __restrict__ l0,
              const double* __restrict__ q, int L, int l_min, int p,
              const double* __restrict__ C, const double* __restrict__ v,
-             const double* __restrict__ lf, int mode, double* __restrict__ panel) {
+             const double* __restrict__ lf, const double* __restrict__ fl, int mode,
+             double* __restrict__ panel) {
     extern __shared__ double zs[];  // [nrows][PANEL_JC]: zm of (row, j) for the current chunk
     const MgTile tl = tiles[blockIdx.x];
     const int kt = (tl.jhi - tl.jlo + RUN_BK) / RUN_BK * RUN_BK;
@@ -123,7 +124,9 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
                 if (ZT) {
                     z = ZT[zoff[tl.row0 + rr] - zbase + (j - rw.jlo)];
                 } else {
-                    z = zm_weight(mode, l0[rw.par] + 2 * j, rw.l2, rw.l3, C, v, l_min, lf);
+                    const int l1 = l0[rw.par] + 2 * j;
+                    z = mode == 0 ? zm_gosper_fast(l1, rw.l2, rw.l3, fl, l_min)
+                                  : zm_weight(mode, l1, rw.l2, rw.l3, C, v, l_min, lf);
                 }
             }
             zs[rr * PANEL_JC + jl] = z;
@@ -204,26 +207,46 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
     const int64_t ldb = (int64_t)p * Nxw;
     RunItems items{tiles, poff, panel, rows, WQB, wbase, wrows, (int)((ldb + RUN_TN - 1) / RUN_TN)};
     const int nitems = ntiles * items.NB;
+    const int64_t pp = (int64_t)p * p;
+    const int XB = NxP / X_BK;
     RunPipeP::run(blockIdx.x, gridDim.x, nitems, items, [&](int it, const Acc<CfgRun>& acc) {
         const int ti = it / items.NB, nb = it - ti * items.NB;
         const MgTile tl = tiles[ti];
         const int n0 = nb * RUN_TN;
         const int64_t hbase = (int64_t)(tl.row0 - row_base) * p + tl.c0;  // H row of slot 0
-        acc_foreach_pair<CfgRun>(acc, [&](int m, int n, double v0, double v1) {
-            const int gn = n0 + n;
-            if (m < tl.nslots && gn < ldb) {
-                const int cp = gn / Nxw, x = gn - cp * Nxw;  // Nxw even: (gn, gn+1) share c'
-                const int64_t slot = hbase + m, rr = slot / p;
-                const int c = (int)(slot - rr * p);
-                double* h = H + ((rr * (NxP / X_BK) + x / X_BK) * (p * p) + c * p + cp) * X_LDK +
-                            (x & (X_BK - 1));
-                if (x + 1 < Nx) {
-                    *reinterpret_cast<double2*>(h) = make_double2(v0, v1);
-                } else if (x < Nx) {
-                    h[0] = v0;
+        // Per-thread offsets, computed once per item (no divisions in the store loop):
+        // slot (rr, c) -> (rr*XB*pp + c*p)*X_LDK ; column gn = c'*Nxw + x ->
+        // ((x/32)*pp + c')*X_LDK + x%32   (Nxw even: columns gn, gn+1 share c' and x-block)
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int wm = (warp / CfgRun::WARPS_N) * (8 * CfgRun::FM) + (lane >> 2);
+        const int wn = (warp % CfgRun::WARPS_N) * (8 * CfgRun::FN) + 2 * (lane & 3);
+        int64_t roff[CfgRun::FM];
+        bool rok[CfgRun::FM];
+#pragma unroll
+        for (int fm = 0; fm < CfgRun::FM; ++fm) {
+            const int m = wm + fm * 8;
+            const int64_t slot = hbase + m, rr = slot / p;
+            rok[fm] = m < tl.nslots;
+            roff[fm] = (rr * XB * pp + (slot - rr * p) * p) * X_LDK;
+        }
+#pragma unroll
+        for (int fn = 0; fn < CfgRun::FN; ++fn) {
+            const int gn = n0 + wn + fn * 8;
+            const int cp = gn / Nxw, x = gn - cp * Nxw;
+            const bool both = gn < ldb && x + 1 < Nx, one = gn < ldb && x < Nx;
+            const int64_t coff = ((int64_t)(x / X_BK) * pp + cp) * X_LDK + (x & (X_BK - 1));
+#pragma unroll
+            for (int fm = 0; fm < CfgRun::FM; ++fm) {
+                if (!rok[fm]) continue;
+                double* h = H + roff[fm] + coff;
+                if (both) {
+                    *reinterpret_cast<double2*>(h) =
+                        make_double2(acc.c[fm][fn][0], acc.c[fm][fn][1]);
+                } else if (one) {
+                    h[0] = acc.c[fm][fn][0];
                 }
             }
-        });
+        }
     }, smem);
 }
 
@@ -571,6 +594,12 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
     P->hv.assign(v, v + L);
 
     P->q.upload(q, (size_t)p * L);
+    {
+        std::vector<double> fl(L);
+        for (int i = 0; i < L; ++i)
+            fl[i] = (2.0 * (l_min + i) + 1.0) / (v[i] * std::sqrt(C[i]));
+        P->fl.upload(fl.data(), L);
+    }
     P->C.upload(C, L);
     P->v.upload(v, L);
     P->wr2.upload(wr2, Nx);
@@ -831,7 +860,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             k_run_panels<<<tl - tf, PANEL_THREADS, max_tile_rows * PANEL_JC * sizeof(double),
                            st>>>(P->sc->tiles.p + tf, P->sc->rows.p, P->sc->poff.p + tf, P->sc->zoff.p, zbase, zt,
                                  l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p,
-                                 P->h2_mode, P->sc->panel.p);
+                                 P->fl.p, P->h2_mode, P->sc->panel.p);
             MG_LAUNCHED();
             {
                 dim3 gs(ceil_div(P2, PP_CHUNK), nb);

@@ -43,7 +43,7 @@ struct mg_plan {
     int64_t wbase[2] = {0, 0};  // WQB offset of each parity class
     int wrows[2] = {0, 0};      // WQB rows per column block of each class (+ zero rows)
     int nclass[2] = {0, 0};  // number of l in each parity class
-    mg::DBuf<double> q, QT, WQT, C, v, lf, wr2;
+    mg::DBuf<double> q, QT, WQT, C, v, lf, wr2, fl;
     mg::DBuf<int> modes;  // [nm][3]
     // scratch
     mg::DBuf<double> gamma;     // Γ of the last execute (owned by the plan)
