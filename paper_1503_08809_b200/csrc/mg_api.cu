@@ -25,6 +25,19 @@ void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int N
                  const double* mu_w, const double* wr2, double* gamma_host);
 
 static thread_local std::string g_last_error;
+
+void ensure_pool_configured() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t threshold = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    done[dev] = true;
+}
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 DeviceGuard::DeviceGuard(int device) {
@@ -162,11 +175,8 @@ int mg_plan_execute(mg_plan* P, int l2_begin, int l2_end, double* gamma_dev, voi
         MG_REQUIRE(P, "null plan");
         DeviceGuard g(P->device);
         if (l2_end < 0) l2_end = P->l_max + 1;
-        int s[3] = {P->l_min, 0, 0}, e[3] = {P->l_max + 1, 0, 0};
-        std::vector<MgRow> rows;
-        build_rows(P, l2_begin, l2_end, s, e, rows);
         cudaStream_t st = (cudaStream_t)stream;
-        execute_rows(P, rows, st);
+        execute_slab(P, l2_begin, l2_end, st);
         if (gamma_dev)
             MG_CUDA(cudaMemcpyAsync(gamma_dev, P->gamma.p, (size_t)P->nm * P->nm * sizeof(double),
                                     cudaMemcpyDeviceToDevice, st));
@@ -257,10 +267,7 @@ int mg_gamma_sep_slab(const double* q, const double* qt, const double* C, const 
     return guarded([&] {
         gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, device, gamma,
                      [&](mg_plan* P) {
-                         int s[3] = {l_min, 0, 0}, e[3] = {l_max + 1, 0, 0};
-                         std::vector<MgRow> rows;
-                         build_rows(P, l2_begin, l2_end < 0 ? l_max + 1 : l2_end, s, e, rows);
-                         execute_rows(P, rows, 0);
+                         execute_slab(P, l2_begin, l2_end < 0 ? l_max + 1 : l2_end, 0);
                      });
     });
 }

@@ -21,6 +21,11 @@ struct Error : std::runtime_error {
 
 void set_last_error(const std::string& msg);
 
+// Device memory comes from the device's stream-ordered pool with an unbounded release
+// threshold: freeing a plan's tables returns them to the pool instead of the driver, so the
+// one-shot drop-in call does not pay cudaMalloc/cudaFree (which synchronise) every time.
+void ensure_pool_configured();
+
 [[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
 
 inline void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
@@ -66,14 +71,15 @@ struct DBuf {
     void alloc(size_t count) {
         release();
         if (count == 0) return;
-        MG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        ensure_pool_configured();
+        MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), 0));
         n = count;
     }
     void ensure(size_t count) {
         if (count > n) alloc(count);
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, 0);
         p = nullptr;
         n = 0;
     }
@@ -87,6 +93,7 @@ struct DBuf {
 };
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 }  // namespace mg

@@ -717,26 +717,22 @@ static void prof_collect(mg_plan* P) {
     P->prof_tags.clear();
 }
 
-static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
-                         const std::vector<int64_t>& hzoff, cudaStream_t st,
-                         const int32_t* dt1, const int32_t* dt2, const int32_t* dt3,
-                         const int64_t* dpos, const double* ddup,
-                         const std::vector<int64_t>* tri_of_row) {
-    const int p = P->p, NxP = P->NxP, P2 = P->P2, nm = P->nm;
+// Host-side batch preparation (tiles, panel offsets, uploads of the row/tile tables).  The
+// result is cached in the plan (P->prep) and reused while the same slab is executed again.
+static void prepare_batches(mg_plan* P, const std::vector<MgRow>& hrows,
+                            const std::vector<int64_t>& hzoff, cudaStream_t st) {
+    const int p = P->p;
     const int64_t nrows = (int64_t)hrows.size();
-    if (!P->nb1) choose_batches(P);
-    const int nb1 = P->nb1, nb3 = P->nb3;
-    const int pp = p * p;
-    const int ncols = p * nm;
-    const int64_t ldr = round_up(ncols, 2);
-    const int ldq = (int)round_up(P2, 2);
-
+    const int nb1 = P->nb1;
+    MgPrepared& pre = P->prep;
     // tiles: 128 consecutive (row, c) slots of one (l2, par) group (rows may straddle two
     // tiles), per nb1-batch; each tile owns a k-major A panel of round_up(window, BK) x 128.
-    std::vector<MgTile> tiles;
+    std::vector<MgTile>& tiles = pre.tiles;
     std::vector<int64_t> poff;      // panel offset of each tile, relative to its batch
-    std::vector<int> tile_first;    // per nb1 batch
+    std::vector<int>& tile_first = pre.tile_first;
     std::vector<int64_t> panel_len; // per nb1 batch
+    tiles.clear();
+    tile_first.clear();
     int max_tile_rows = 1;
     for (int64_t b1 = 0; b1 < nrows; b1 += nb1) {
         int64_t e1 = std::min<int64_t>(b1 + nb1, nrows);
@@ -773,16 +769,44 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     }
     tile_first.push_back((int)tiles.size());
 
-    P->sc->rows.upload(hrows.data(), hrows.size(), st);
-    P->sc->zoff.upload(hzoff.data(), hzoff.size(), st);
-    P->sc->tiles.upload(tiles.data(), tiles.size(), st);
-    P->sc->poff.upload(poff.data(), poff.size(), st);
+    pre.rows.upload(hrows.data(), hrows.size(), st);
+    pre.zoff.upload(hzoff.data(), hzoff.size(), st);
+    pre.tiles_d.upload(tiles.data(), tiles.size(), st);
+    pre.poff.upload(poff.data(), poff.size(), st);
     int64_t maxzt = 1, maxpanel = 1;
     for (size_t bi = 0; bi + 1 < tile_first.size(); ++bi) {
         int64_t b1 = bi * (int64_t)nb1, e1 = std::min<int64_t>(b1 + nb1, nrows);
         maxzt = std::max(maxzt, hzoff[e1] - hzoff[b1]);
         maxpanel = std::max(maxpanel, panel_len[bi]);
     }
+    pre.max_tile_rows = max_tile_rows;
+    pre.maxzt = maxzt;
+    pre.maxpanel = maxpanel;
+    pre.nrows = nrows;
+    pre.valid = true;
+}
+
+static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
+                         const std::vector<int64_t>& hzoff, cudaStream_t st,
+                         const int32_t* dt1, const int32_t* dt2, const int32_t* dt3,
+                         const int64_t* dpos, const double* ddup,
+                         const std::vector<int64_t>* tri_of_row) {
+    const int p = P->p, NxP = P->NxP, P2 = P->P2, nm = P->nm;
+    const int64_t nrows = (int64_t)hrows.size();
+    if (!P->nb1) choose_batches(P);
+    const int nb1 = P->nb1, nb3 = P->nb3;
+    const int pp = p * p;
+    const int ncols = p * nm;
+    const int64_t ldr = round_up(ncols, 2);
+    const int ldq = (int)round_up(P2, 2);
+
+    MgPrepared& pre = P->prep;
+    if (!pre.valid) prepare_batches(P, hrows, hzoff, st);
+    const std::vector<MgTile>& tiles = pre.tiles;
+    const std::vector<int>& tile_first = pre.tile_first;
+    const int max_tile_rows = pre.max_tile_rows;
+    const int64_t maxzt = pre.maxzt, maxpanel = pre.maxpanel;
+    (void)tiles;
     if (dt1) P->sc->ZT.ensure(maxzt);
     P->sc->panel.ensure(maxpanel);
     const size_t hsize = (size_t)nb1 * pp * (NxP / X_BK) * X_LDK;
@@ -858,19 +882,19 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             int tf = tile_first[bidx], tl = tile_first[bidx + 1];
             prof_mark(P, 0, st);
             k_run_panels<<<tl - tf, PANEL_THREADS, max_tile_rows * PANEL_JC * sizeof(double),
-                           st>>>(P->sc->tiles.p + tf, P->sc->rows.p, P->sc->poff.p + tf, P->sc->zoff.p, zbase, zt,
+                           st>>>(P->prep.tiles_d.p + tf, P->prep.rows.p, P->prep.poff.p + tf, P->prep.zoff.p, zbase, zt,
                                  l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p,
                                  P->fl.p, P->h2_mode, P->sc->panel.p);
             MG_LAUNCHED();
             {
                 dim3 gs(ceil_div(P2, PP_CHUNK), nb);
-                k_pair_products<<<gs, 256, 0, st>>>(P->sc->rows.p, (int)b1, P->QT.p, p, P2, NxP,
+                k_pair_products<<<gs, 256, 0, st>>>(P->prep.rows.p, (int)b1, P->QT.p, p, P2, NxP,
                                                     P->l_min, P->sc->S.p);
                 MG_LAUNCHED();
             }
             prof_mark(P, 1, st);
             k_run_contract<<<num_sms, RunPipeP::THREADS, smem_run, st>>>(
-                P->sc->tiles.p + tf, tl - tf, P->sc->poff.p + tf, P->sc->panel.p, (int)b1, P->sc->rows.p,
+                P->prep.tiles_d.p + tf, tl - tf, P->prep.poff.p + tf, P->sc->panel.p, (int)b1, P->prep.rows.p,
                 P->WQT.p, p, P->Nx, P->Nxw, NxP, make_longlong2(P->wbase[0], P->wbase[1]),
                 make_int2(P->wrows[0], P->wrows[1]), P->sc->H.p);
             MG_LAUNCHED();
@@ -894,7 +918,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         const int n3 = (int)(e3 - b3);
         prof_mark(P, 3, st);
         dim3 gg(std::min(ceil_div(ncols, 256), 64), n3);
-        k_gather<<<gg, 256, 0, st>>>(P->sc->rows.p + b3, P->sc->G.p, P->modes.p, P->q.p, P->L, P->l_min,
+        k_gather<<<gg, 256, 0, st>>>(P->prep.rows.p + b3, P->sc->G.p, P->modes.p, P->q.p, P->L, P->l_min,
                                      p, P2, nm, ldr, ldq, P->sc->R.p, P->sc->Sq.p);
         MG_LAUNCHED();
         const int per = (int)round_up(ceil_div(n3, nsplit), PAIR_BK);
@@ -920,18 +944,45 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     prof_collect(P);
 }
 
+static void zero_result(mg_plan* P, cudaStream_t st) {
+    P->gamma.ensure((size_t)P->nm * P->nm);
+    MG_CUDA(cudaMemsetAsync(P->gamma.p, 0, (size_t)P->nm * P->nm * sizeof(double), st));
+    P->flops_run = P->flops_x = P->flops_pair = 0;
+    P->launches = 0;
+}
+
+static void set_rows(mg_plan* P, std::vector<MgRow>&& rows) {
+    MgPrepared& pre = P->prep;
+    pre.valid = false;
+    pre.key_a = pre.key_b = -1;
+    pre.hrows = std::move(rows);
+    pre.hzoff.assign(pre.hrows.size() + 1, 0);
+    for (size_t i = 0; i < pre.hrows.size(); ++i)
+        pre.hzoff[i + 1] = pre.hzoff[i] + (pre.hrows[i].jhi - pre.hrows[i].jlo + 1);
+}
+
 void execute_rows(mg_plan* P, const std::vector<MgRow>& rows, cudaStream_t st) {
-    std::vector<int64_t> zoff(rows.size() + 1, 0);
-    for (size_t i = 0; i < rows.size(); ++i)
-        zoff[i + 1] = zoff[i] + (rows[i].jhi - rows[i].jlo + 1);
-    if (rows.empty()) {
-        P->gamma.ensure((size_t)P->nm * P->nm);
-        MG_CUDA(cudaMemsetAsync(P->gamma.p, 0, (size_t)P->nm * P->nm * sizeof(double), st));
-        P->flops_run = P->flops_x = P->flops_pair = 0;
-        P->launches = 0;
-        return;
+    set_rows(P, std::vector<MgRow>(rows));
+    if (P->prep.hrows.empty()) return zero_result(P, st);
+    run_pipeline(P, P->prep.hrows, P->prep.hzoff, st, nullptr, nullptr, nullptr, nullptr,
+                 nullptr, nullptr);
+}
+
+// l2 slab [l2a, l2b) of the full domain; the batch tables are reused when the same slab is
+// executed again on this plan (bench steps, multi-GPU ranks).
+void execute_slab(mg_plan* P, int l2a, int l2b, cudaStream_t st) {
+    MgPrepared& pre = P->prep;
+    if (!(pre.valid && pre.key_a == l2a && pre.key_b == l2b)) {
+        int s[3] = {P->l_min, 0, 0}, e[3] = {P->l_max + 1, 0, 0};
+        std::vector<MgRow> rows;
+        build_rows(P, l2a, l2b, s, e, rows);
+        set_rows(P, std::move(rows));
     }
-    run_pipeline(P, rows, zoff, st, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (pre.hrows.empty()) return zero_result(P, st);
+    run_pipeline(P, pre.hrows, pre.hzoff, st, nullptr, nullptr, nullptr, nullptr, nullptr,
+                 nullptr);
+    pre.key_a = l2a;
+    pre.key_b = l2b;
 }
 
 void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
@@ -984,6 +1035,8 @@ void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int
         execute_rows(P, rows, st);
         return;
     }
+    P->prep.valid = false;
+    P->prep.key_a = P->prep.key_b = -1;
     DBuf<int32_t> d1, d2, d3;
     DBuf<int64_t> dp;
     DBuf<double> dd;
@@ -993,6 +1046,7 @@ void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int
     dp.upload(pos.data(), pos.size(), st);
     dd.upload(dup.data(), dup.size(), st);
     run_pipeline(P, rows, zoff, st, d1.p, d2.p, d3.p, dp.p, dd.p, &tri_of_row);
+    P->prep.valid = false;  // tables belong to this explicit triple list
 }
 
 // ------------------------------------------------------------------------------------------

@@ -28,10 +28,24 @@ constexpr int MG_NPROF = 6;
 // not re-entrant (documented in include/modal_b200.h), so sharing is safe.
 struct MgScratch {
     mg::DBuf<double> ZT, panel, H, S, G, R, Sq, Z;
-    mg::DBuf<int64_t> poff;
+};
+
+// Prepared (host-built, device-uploaded) batch tables of one slab; cached in the plan so a
+// repeated execute of the same slab skips the host preparation.
+struct MgPrepared {
+    bool valid = false;
+    int key_a = -1, key_b = -1;
+    int64_t nrows = 0;
+    std::vector<MgRow> hrows;
+    std::vector<int64_t> hzoff;
+    std::vector<MgTile> tiles;
+    std::vector<int> tile_first;
+    int max_tile_rows = 1;
+    int64_t maxzt = 1, maxpanel = 1;
     mg::DBuf<MgRow> rows;
     mg::DBuf<int64_t> zoff;
-    mg::DBuf<MgTile> tiles;
+    mg::DBuf<MgTile> tiles_d;
+    mg::DBuf<int64_t> poff;
 };
 
 struct mg_plan {
@@ -48,6 +62,7 @@ struct mg_plan {
     // scratch
     mg::DBuf<double> gamma;     // Γ of the last execute (owned by the plan)
     MgScratch* sc = nullptr;    // per-device scratch pool (shared by plans on the device)
+    MgPrepared prep;            // cached batch tables of the last executed slab
     int nb1 = 0, nb3 = 0;  // rows per run/x-contraction batch, rows per pair-contraction batch
     // stats of the last execute
     double flops_run = 0, flops_x = 0, flops_pair = 0;
@@ -74,6 +89,7 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
 void build_rows(const mg_plan* P, int l2a, int l2b, const int* s, const int* e,
                 std::vector<MgRow>& rows);
 void execute_rows(mg_plan* P, const std::vector<MgRow>& rows, cudaStream_t st);
+void execute_slab(mg_plan* P, int l2a, int l2b, cudaStream_t st);
 void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
                      int64_t count, cudaStream_t st);
 void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l2,
