@@ -1188,6 +1188,178 @@ k_nonsep(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
     for (int i = threadIdx.x; i < nm; i += blockDim.x) partial[(int64_t)blockIdx.x * nm + i] = b_acc[i];
 }
 
+// Faster pointwise kernel (p <= 16): per (triple, x) each thread stages q̃ at l1, l2, l3 and
+// the pair sums S_ab(x) = q̃_a(x,l2)q̃_b(x,l3) + q̃_b(x,l2)q̃_a(x,l3) in its own shared-memory
+// column, then sums the modes pointwise: B(t,x) = Σ_n' α_n' [q̃_k'(l1) S_i'j' + q̃_j'(l1) S_i'k'
+// + q̃_i'(l1) S_j'k'] (the 6-permutation product, no factoring through Γ).
+constexpr int NS2_THREADS = 128;
+
+__global__ void __launch_bounds__(NS2_THREADS)
+k_nonsep2(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
+          const int32_t* __restrict__ t3, const double* __restrict__ W, int64_t count,
+          const double* __restrict__ QT, const double* __restrict__ wr2,
+          const double* __restrict__ q, const double* __restrict__ C, const double* __restrict__ v,
+          const double* __restrict__ lf, int mode, const double* __restrict__ alpha,
+          const int* __restrict__ modes, int p, int nm, int Nx, int NxP, int L, int l_min,
+          double* __restrict__ partial) {
+    extern __shared__ double sh[];
+    const int P2 = p * (p + 1) / 2;
+    double* col = sh;                                   // [(3p + P2)][NS2_THREADS]
+    double* b_acc = col + (3 * p + P2) * NS2_THREADS;   // [nm]
+    double* al = b_acc + nm;                            // [nm]
+    double* red = al + nm;                              // [NS2_THREADS/32]
+    int* md = reinterpret_cast<int*>(red + NS2_THREADS / 32);  // [nm][6]: i j k, ij ik jk
+    for (int i = threadIdx.x; i < nm; i += blockDim.x) {
+        b_acc[i] = 0.0;
+        al[i] = alpha[i];
+        const int a = modes[3 * i], b = modes[3 * i + 1], c = modes[3 * i + 2];
+        md[6 * i] = a; md[6 * i + 1] = b; md[6 * i + 2] = c;
+        md[6 * i + 3] = pair_idx(a, b); md[6 * i + 4] = pair_idx(a, c); md[6 * i + 5] = pair_idx(b, c);
+    }
+    __syncthreads();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* q1 = col;                       // q̃(l1)[c]  at q1[c*T + tid]
+    double* q2 = col + p * NS2_THREADS;
+    double* q3 = col + 2 * p * NS2_THREADS;
+    double* S = col + 3 * p * NS2_THREADS;  // S[pair*T + tid]
+    for (int64_t t = blockIdx.x; t < count; t += gridDim.x) {
+        const int a1 = t1[t], a2 = t2[t], a3 = t3[t];
+        const double* g1 = QT + (int64_t)(a1 - l_min) * p * NxP;
+        const double* g2 = QT + (int64_t)(a2 - l_min) * p * NxP;
+        const double* g3 = QT + (int64_t)(a3 - l_min) * p * NxP;
+        double xs = 0.0;
+        for (int x = tid; x < Nx; x += NS2_THREADS) {
+            for (int c = 0; c < p; ++c) {
+                q1[c * NS2_THREADS + tid] = g1[c * NxP + x];
+                q2[c * NS2_THREADS + tid] = g2[c * NxP + x];
+                q3[c * NS2_THREADS + tid] = g3[c * NxP + x];
+            }
+            for (int b = 0, pr = 0; b < p; ++b) {
+                const double b2 = q2[b * NS2_THREADS + tid], b3 = q3[b * NS2_THREADS + tid];
+                for (int a = 0; a <= b; ++a, ++pr)
+                    S[pr * NS2_THREADS + tid] =
+                        q2[a * NS2_THREADS + tid] * b3 + b2 * q3[a * NS2_THREADS + tid];
+            }
+            double Bx = 0.0;
+            for (int m = 0; m < nm; ++m) {
+                const int* e = md + 6 * m;
+                const double f = q1[e[2] * NS2_THREADS + tid] * S[e[3] * NS2_THREADS + tid] +
+                                 q1[e[1] * NS2_THREADS + tid] * S[e[4] * NS2_THREADS + tid] +
+                                 q1[e[0] * NS2_THREADS + tid] * S[e[5] * NS2_THREADS + tid];
+                Bx += al[m] * f;
+            }
+            xs += wr2[x] * Bx;
+        }
+        for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+        if (lane == 0) red[warp] = xs;
+        __syncthreads();
+        double X = 0.0;
+        for (int w = 0; w < NS2_THREADS / 32; ++w) X += red[w];
+        const double wz = W[t] * zm_weight(mode, a1, a2, a3, C, v, l_min, lf) * X;
+        for (int m = tid; m < nm; m += NS2_THREADS) {
+            const int i = md[6 * m], j = md[6 * m + 1], k = md[6 * m + 2];
+            const double* qi = q + (int64_t)i * L - l_min;
+            const double* qj = q + (int64_t)j * L - l_min;
+            const double* qk = q + (int64_t)k * L - l_min;
+            const double P = qi[a1] * (qj[a2] * qk[a3] + qk[a2] * qj[a3]) +
+                             qj[a1] * (qi[a2] * qk[a3] + qk[a2] * qi[a3]) +
+                             qk[a1] * (qi[a2] * qj[a3] + qj[a2] * qi[a3]);
+            b_acc[m] += wz * P;
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < nm; i += NS2_THREADS) partial[(int64_t)blockIdx.x * nm + i] = b_acc[i];
+}
+
+// Register-resident pointwise kernel for a compile-time basis size P (config 3: P = 8).
+// Per (triple, x): q̃(l1)[c] and the pair sums S_ab(x) live in registers; the mode sum walks
+// every ordered triple i <= j <= k < P with compile-time indices and a dense α table
+// (zero for triples absent from the mapping, read as shared-memory broadcasts):
+//   B(t,x) = Σ_{i<=j<=k} α_ijk [q̃_k(l1) S_ij + q̃_j(l1) S_ik + q̃_i(l1) S_jk]
+template <int P>
+__global__ void __launch_bounds__(128)
+k_nonsep_reg(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
+             const int32_t* __restrict__ t3, const double* __restrict__ W, int64_t count,
+             const double* __restrict__ QT, const double* __restrict__ wr2,
+             const double* __restrict__ q, const double* __restrict__ C,
+             const double* __restrict__ v, const double* __restrict__ lf, int mode,
+             const double* __restrict__ alpha_dense, const int* __restrict__ modes, int nm,
+             int Nx, int NxP, int L, int l_min, double* __restrict__ partial) {
+    constexpr int NT = P * (P + 1) * (P + 2) / 6;
+    constexpr int P2 = P * (P + 1) / 2;
+    extern __shared__ double sh[];
+    double* al = sh;                 // [NT] dense α in (k, j, i) order
+    double* b_acc = al + NT;         // [nm]
+    double* red = b_acc + nm;        // [4]
+    for (int i = threadIdx.x; i < NT; i += blockDim.x) al[i] = alpha_dense[i];
+    for (int i = threadIdx.x; i < nm; i += blockDim.x) b_acc[i] = 0.0;
+    __syncthreads();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t t = blockIdx.x; t < count; t += gridDim.x) {
+        const int a1 = t1[t], a2 = t2[t], a3 = t3[t];
+        const double* g1 = QT + (int64_t)(a1 - l_min) * P * NxP;
+        const double* g2 = QT + (int64_t)(a2 - l_min) * P * NxP;
+        const double* g3 = QT + (int64_t)(a3 - l_min) * P * NxP;
+        double xs = 0.0;
+        for (int x = tid; x < Nx; x += blockDim.x) {
+            double q1[P], q2[P], q3[P], S[P2];
+#pragma unroll
+            for (int c = 0; c < P; ++c) {
+                q1[c] = g1[c * NxP + x];
+                q2[c] = g2[c * NxP + x];
+                q3[c] = g3[c * NxP + x];
+            }
+#pragma unroll
+            for (int b = 0; b < P; ++b)
+#pragma unroll
+                for (int a = 0; a <= b; ++a) S[b * (b + 1) / 2 + a] = q2[a] * q3[b] + q2[b] * q3[a];
+            double Bx = 0.0;
+            int n = 0;
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+#pragma unroll
+                for (int j = 0; j <= k; ++j)
+#pragma unroll
+                    for (int i = 0; i <= j; ++i, ++n) {
+                        const double f = q1[k] * S[j * (j + 1) / 2 + i] +
+                                         q1[j] * S[k * (k + 1) / 2 + i] +
+                                         q1[i] * S[k * (k + 1) / 2 + j];
+                        Bx += al[n] * f;
+                    }
+            xs += wr2[x] * Bx;
+        }
+        for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+        if (lane == 0) red[warp] = xs;
+        __syncthreads();
+        const double X = red[0] + red[1] + red[2] + red[3];
+        const double wz = W[t] * zm_weight(mode, a1, a2, a3, C, v, l_min, lf) * X;
+        for (int m = tid; m < nm; m += blockDim.x) {
+            const int i = modes[3 * m], j = modes[3 * m + 1], k = modes[3 * m + 2];
+            const double* qi = q + (int64_t)i * L - l_min;
+            const double* qj = q + (int64_t)j * L - l_min;
+            const double* qk = q + (int64_t)k * L - l_min;
+            const double Pm = qi[a1] * (qj[a2] * qk[a3] + qk[a2] * qj[a3]) +
+                              qj[a1] * (qi[a2] * qk[a3] + qk[a2] * qi[a3]) +
+                              qk[a1] * (qi[a2] * qj[a3] + qj[a2] * qi[a3]);
+            b_acc[m] += wz * Pm;
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < nm; i += blockDim.x) partial[(int64_t)blockIdx.x * nm + i] = b_acc[i];
+}
+
+template <int P>
+static void launch_nonsep_reg(int nblocks, cudaStream_t st, const int32_t* d1, const int32_t* d2,
+                              const int32_t* d3, const double* dW, int64_t count, mg_plan* Pl,
+                              const double* alpha_dense, double* part) {
+    constexpr int NT = P * (P + 1) * (P + 2) / 6;
+    const size_t shm = (size_t)(NT + Pl->nm + 4) * sizeof(double);
+    k_nonsep_reg<P><<<nblocks, 128, shm, st>>>(d1, d2, d3, dW, count, Pl->QT.p, Pl->wr2.p,
+                                                Pl->q.p, Pl->C.p, Pl->v.p, Pl->lf.p, Pl->h2_mode,
+                                                alpha_dense, Pl->modes.p, Pl->nm, Pl->Nx,
+                                                Pl->NxP, Pl->L, Pl->l_min, part);
+}
+
 __global__ void k_sum_partials(const double* __restrict__ partial, int nblocks, int nm,
                                double* __restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1214,13 +1386,44 @@ void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l
     const int nblocks = 148 * 8;
     DBuf<double> part((size_t)nblocks * nm);
     dout.alloc(nm);
-    size_t shm = (size_t)nm * 8 + NS_THREADS / 32 * 8 + (3 * nm + 1) * 4 + 8 + (size_t)nm * 8;
-    if (shm > 48 * 1024)
-        MG_CUDA(cudaFuncSetAttribute(k_nonsep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_nonsep<<<nblocks, NS_THREADS, shm, st>>>(d1.p, d2.p, d3.p, dW.p, count, P->QT.p, P->wr2.p,
-                                                P->q.p, P->C.p, P->v.p, P->lf.p, P->h2_mode,
-                                                dal.p, P->modes.p, P->p, nm, P->Nx, P->NxP,
-                                                P->L, P->l_min, part.p);
+    const int p = P->p, P2 = p * (p + 1) / 2;
+    const size_t shm2 = (size_t)(3 * p + P2) * NS2_THREADS * 8 + 2 * (size_t)nm * 8 +
+                        NS2_THREADS / 32 * 8 + (size_t)6 * nm * 4;
+    // dense α over all ordered triples (k, j, i order), zero where the mapping has no mode
+    std::vector<double> ad((size_t)p * (p + 1) * (p + 2) / 6, 0.0);
+    {
+        std::vector<int> md(3 * (size_t)nm);
+        MG_CUDA(cudaMemcpy(md.data(), P->modes.p, md.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int m = 0; m < nm; ++m) {
+            const int i = md[3 * m], j = md[3 * m + 1], k = md[3 * m + 2];
+            ad[(size_t)k * (k + 1) * (k + 2) / 6 + j * (j + 1) / 2 + i] = alpha[m];
+        }
+    }
+    DBuf<double> dad;
+    dad.upload(ad.data(), ad.size(), st);
+    const bool reg = p == 4 || p == 6 || p == 8 || p == 10;
+    if (reg) {
+        switch (p) {
+            case 4: launch_nonsep_reg<4>(nblocks, st, d1.p, d2.p, d3.p, dW.p, count, P, dad.p, part.p); break;
+            case 6: launch_nonsep_reg<6>(nblocks, st, d1.p, d2.p, d3.p, dW.p, count, P, dad.p, part.p); break;
+            case 8: launch_nonsep_reg<8>(nblocks, st, d1.p, d2.p, d3.p, dW.p, count, P, dad.p, part.p); break;
+            default: launch_nonsep_reg<10>(nblocks, st, d1.p, d2.p, d3.p, dW.p, count, P, dad.p, part.p); break;
+        }
+    } else if (shm2 <= 200 * 1024) {
+        MG_CUDA(cudaFuncSetAttribute(k_nonsep2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)shm2));
+        k_nonsep2<<<nblocks, NS2_THREADS, shm2, st>>>(
+            d1.p, d2.p, d3.p, dW.p, count, P->QT.p, P->wr2.p, P->q.p, P->C.p, P->v.p, P->lf.p,
+            P->h2_mode, dal.p, P->modes.p, P->p, nm, P->Nx, P->NxP, P->L, P->l_min, part.p);
+    } else {
+        size_t shm = (size_t)nm * 8 + NS_THREADS / 32 * 8 + (3 * nm + 1) * 4 + 8 + (size_t)nm * 8;
+        if (shm > 48 * 1024)
+            MG_CUDA(cudaFuncSetAttribute(k_nonsep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)shm));
+        k_nonsep<<<nblocks, NS_THREADS, shm, st>>>(
+            d1.p, d2.p, d3.p, dW.p, count, P->QT.p, P->wr2.p, P->q.p, P->C.p, P->v.p, P->lf.p,
+            P->h2_mode, dal.p, P->modes.p, P->p, nm, P->Nx, P->NxP, P->L, P->l_min, part.p);
+    }
     MG_LAUNCHED();
     k_sum_partials<<<(nm + 127) / 128, 128, 0, st>>>(part.p, nblocks, nm, dout.p);
     MG_LAUNCHED();

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from .engine3d import _base_meta
+from .engine3d import _FP_POOL, _meta_dict
 from .gamma import GammaMatrix
 from .quadrature import x_weights
 
@@ -69,12 +69,14 @@ def gamma_nonsep(tables, mapping, grid, alpha, domain: SparseDomain, h2_mode: st
     W = np.ascontiguousarray(domain.weight, np.float64)
     n = entries.shape[0]
     b = np.zeros(n)
+    fp = _FP_POOL.submit(lambda: (tables.fingerprint(), grid.fingerprint(),
+                                  mapping.fingerprint()))   # overlaps the GPU call
     nat.check(nat.lib().mg_gamma_nonsep(
         nat.ptr(q), nat.ptr(qt), nat.ptr(C), nat.ptr(v), nat.ptr(wr2), nat.ptr(entries),
         q.shape[0], qt.shape[1], n, int(tables.l_min), int(tables.l_max), nat.MG_H2[h2_mode],
         nat.ptr(alpha), nat.ptr(l1), nat.ptr(l2), nat.ptr(l3), nat.ptr(W), int(l1.size),
         int(device), nat.ptr(b)))
-    meta = _base_meta(tables, grid, mapping, integrator, h2_mode, 1, 1)
+    meta = _meta_dict(tables, grid, mapping, integrator, h2_mode, 1, 1, *fp.result())
     meta["engine"] = "modal3d-nonsep"
     meta["triples"] = int(l1.size)
     return GammaMatrix(b.reshape(n, 1), meta)
