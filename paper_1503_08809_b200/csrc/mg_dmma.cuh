@@ -1,4 +1,4 @@
-// mg_dmma.cuh — FP64 tensor-core (DMMA) block GEMM with a cp.async multi-stage pipeline.
+// mg_dmma.cuh — FP64 tensor-core (DMMA) block GEMM pipelines for the Γ contractions.
 //
 // Blackwell has no FP64 tcgen05 kind; FP64 tensor math is the legacy `mma.sync ... .f64`
 // path, which ptxas lowers to DMMA.8x8x4 on sm_100a (every f64 mma shape becomes a sequence
@@ -9,11 +9,16 @@
 // fragments, so BM = 8*FM*WARPS_M, BN = 8*FN*WARPS_N.  Operand tiles live in shared memory
 // either k-major (X[k][m], row stride W+4) or m-major (X[m][k], row stride BK+4); both pads
 // keep the fragment reads (lane (g,t) reads element (m0+g, k0+t)) bank-conflict free and
-// rows 16-byte aligned for cp.async.  Tiles are streamed global->shared with cp.async
-// (16-byte chunks, zero-fill outside the matrix) through a STAGES-deep ring.  The A operand
-// may instead be produced per fragment by the producer from staged raw data (a_frag), which
-// is how the x contraction forms its pair products S_ab(x) without a shared-memory pass.
-// Fragments are double-buffered in registers across the k4 steps.
+// rows 16-byte aligned.  Fragments are double-buffered in registers across the k4 steps and
+// all-zero k4 steps of the last k-tile are skipped.  Two pipelines:
+//   Pipe               all threads stream tiles with 16-byte cp.async (zero-fill at edges)
+//                      through a STAGES-deep ring, one CTA barrier per k-tile (pair
+//                      contraction, p = 22 x contraction);
+//   PipeTMA(Persistent) one producer warp moves whole tiles with cp.async.bulk (TMA engine)
+//                      completing on per-stage mbarriers; 15 consumer warps wait on "full",
+//                      release through "empty"; no CTA barrier in the loop; the persistent
+//                      form walks work items so the next item streams in during an epilogue
+//                      (run and x contractions).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -191,13 +196,7 @@ struct Pipe {
 
 
 // ------------------------------------------------------------------------------------------
-// Warp-specialised variant: Cfg::WARPS consumer warps + 1 producer warp.  The producer
-// streams every stage with cp.async and signals a per-stage "full" mbarrier through
-// cp.async.mbarrier.arrive.noinc; consumers wait on "full", run the DMMAs, and release the
-// stage through an "empty" mbarrier (one arrive per consumer warp).  No CTA-wide barrier in
-// the main loop, and the consumers never execute copy/address code.
-// Producer contract: __device__ void issue_warp(int kt, double* As, double* Bs, int lane) const;
-//                    __device__ int kvalid_last() const;
+// mbarrier helpers for the warp-specialised pipelines below
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -216,115 +215,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, int parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity));
 }
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)));
-}
-
-// single-warp tile copies (the producer warp): same layouts as copy_kmajor / copy_mmajor
-template <int BK, int W, class RowPtr>
-__device__ __forceinline__ void warp_copy_kmajor(double* dst, RowPtr&& src_row, int w_valid,
-                                                 int lane) {
-    constexpr int CPR = W / 2, CH = BK * CPR;
-#pragma unroll 4
-    for (int c = lane; c < CH; c += 32) {
-        int k = c / CPR, m = (c % CPR) * 2;
-        const double* s = src_row(k);
-        double* d = dst + k * ld_kmajor(W) + m;
-        int bytes = (s && m < w_valid) ? ((w_valid - m) >= 2 ? 16 : 8) : 0;
-        cp_async16(d, bytes ? s + m : d, bytes);
-    }
-}
-template <int BK, int W, class RowPtr>
-__device__ __forceinline__ void warp_copy_mmajor(double* dst, RowPtr&& src_row, int k_valid,
-                                                 int lane) {
-    constexpr int CPR = BK / 2, CH = W * CPR;
-#pragma unroll 4
-    for (int c = lane; c < CH; c += 32) {
-        int m = c / CPR, k = (c % CPR) * 2;
-        const double* s = src_row(m);
-        double* d = dst + m * ld_mmajor(BK) + k;
-        int bytes = (s && k < k_valid) ? ((k_valid - k) >= 2 ? 16 : 8) : 0;
-        cp_async16(d, bytes ? s + k : d, bytes);
-    }
-}
-
-template <class Cfg, int BK, int STAGES, bool AK, bool BKM>
-struct PipeWS {
-    static constexpr int WARPS = Cfg::WARPS_M * Cfg::WARPS_N;
-    static constexpr int THREADS = Cfg::THREADS + 32;
-    static constexpr int SA = tile_doubles(AK, Cfg::BM, BK);
-    static constexpr int SB = tile_doubles(BKM, Cfg::BN, BK);
-    static constexpr int SS = SA + SB;
-    static constexpr size_t smem_bytes = (size_t)STAGES * SS * sizeof(double) + 2 * STAGES * 8;
-
-    __device__ static bool is_producer() { return (int)(threadIdx.x >> 5) == WARPS; }
-
-    // Returns true in consumer threads (which then own `acc`); the producer returns false.
-    template <class Prod>
-    __device__ static bool run(int ktiles, const Prod& prod, double* smem, Acc<Cfg>& acc) {
-        constexpr int FM = Cfg::FM, FN = Cfg::FN;
-        uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SS);
-        uint64_t* empty = full + STAGES;
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        if (threadIdx.x == 0) {
-            for (int s = 0; s < STAGES; ++s) {
-                mbar_init(full + s, 32);
-                mbar_init(empty + s, WARPS);
-            }
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-        }
-        __syncthreads();
-        if (warp == WARPS) {  // ---------------- producer warp
-            for (int kt = 0; kt < ktiles; ++kt) {
-                const int s = kt % STAGES;
-                if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
-                double* st = smem + s * SS;
-                prod.issue_warp(kt, st, st + SA, lane);
-                cp_async_mbar_arrive(full + s);
-            }
-            cp_async_wait<0>();
-            return false;
-        }
-        // ------------------------------------------------------------- consumer warps
-        const int g = lane >> 2, t = lane & 3;
-        const int wm = (warp / Cfg::WARPS_N) * (8 * FM), wn = (warp % Cfg::WARPS_N) * (8 * FN);
-#pragma unroll
-        for (int mi = 0; mi < FM; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < FN; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
-        for (int kt = 0; kt < ktiles; ++kt) {
-            const int s = kt % STAGES;
-            mbar_wait(full + s, (kt / STAGES) & 1);
-            const double* As = smem + s * SS;
-            const double* Bs = As + SA;
-            double a[2][FM], b[2][FN];
-            auto load_frags = [&](int buf, int k) {
-#pragma unroll
-                for (int mi = 0; mi < FM; ++mi) a[buf][mi] = frag_ld<AK, Cfg::BM, BK>(As, k, wm + mi * 8 + g);
-#pragma unroll
-                for (int ni = 0; ni < FN; ++ni) b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g);
-            };
-            const int nks = kt + 1 < ktiles ? BK / 4 : (prod.kvalid_last() + 3) / 4;
-            load_frags(0, t);
-#pragma unroll
-            for (int ks = 0; ks < BK / 4; ++ks) {
-                if (ks < nks) {
-                    const int cur = ks & 1;
-                    if (ks + 1 < BK / 4) load_frags(cur ^ 1, (ks + 1) * 4 + t);
-#pragma unroll
-                    for (int mi = 0; mi < FM; ++mi)
-#pragma unroll
-                        for (int ni = 0; ni < FN; ++ni)
-                            dmma884(acc.c[mi][ni], a[cur][mi], b[cur][ni]);
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + s);
-        }
-        return true;
-    }
-};
-
 
 // ------------------------------------------------------------------------------------------
 // Bulk-copy (TMA engine) variant of the warp-specialised pipeline.  The producer warp moves
