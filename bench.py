@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--config", default="c1")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-reps", type=int, default=2)
+    ap.add_argument("--e2e-reps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: exchange Γ partials through host memory (lets N ranks share "
@@ -269,7 +269,7 @@ def run_b200(args):
             t1 = time.perf_counter()
             g = gamma3d_matrix(tables, mapping, grid, device=local)
         e2e_t.append(time.perf_counter() - t1)
-    e2e_s = float(np.mean(e2e_t))
+    e2e_s = float(np.median(e2e_t))
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cpu" if gloo else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

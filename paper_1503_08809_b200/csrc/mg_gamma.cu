@@ -84,7 +84,7 @@ __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t*
 // K1a: A panels of the run contraction, one per M-tile, k-major [jl][slot]:
 //   panel[jl][slot=(r,c)] = zm(l1(j), l2_r, l3_r) q_c(l1(j))  (0 outside row r's window)
 // ------------------------------------------------------------------------------------------
-constexpr int RUN_BK = 32, RUN_ST = 3;
+constexpr int RUN_BK = 16, RUN_ST = 6;
 constexpr int X_BK = 32;
 constexpr int X_LDK = X_BK + 4;  // x-blocked S/H row stride: [row][x/32][m][36], smem-identical
 constexpr int PAIR_BK = 32, PAIR_ST = 3;
@@ -94,7 +94,7 @@ using CfgRun = CfgX120;                // run contraction: 15 consumer warps + 1
 using PairPipe = Pipe<Cfg128, PAIR_BK, PAIR_ST, ASrc::KMajor, true, 0>;
 constexpr int RUN_TM = CfgRun::BM;     // (row, c) slots per run tile = A panel width
 static_assert(RUN_TN == CfgRun::BN && RUN_LDB == ld_kmajor(RUN_TM) &&
-                  RUN_LDB == ld_kmajor(RUN_TN) && RUN_BK == 32,
+                  RUN_LDB == ld_kmajor(RUN_TN),
               "bulk-copied run tiles must match the shared-memory layout");
 constexpr int PANEL_THREADS = 256;
 constexpr int PANEL_JC = 32;  // j values per shared-memory weight chunk
