@@ -290,6 +290,15 @@ def run_b200(args):
     achieved = fams[dom] / k_time / 1e12 if k_time > 0 else 0.0
     exec_flops = sum(fams.values())
     step_s = ms / 1e3
+    traffic, traffic_note = None, None
+    tfile = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tfile):
+        tr = json.load(open(tfile)).get(names[dom])
+        if tr:
+            traffic = tr["dram_bytes"]
+            traffic_note = (f"dram read+write bytes of one profiled {names[dom]} launch "
+                            f"({tr['duration_ms']:.2f} ms, config-1 l2 slab [1400,1420)) from "
+                            f"ncu --set full, profiles/r01_ncu_full_c1.txt")
     line = {
         "metric": "Γ projection: (l-triple·x·mode) FP64 updates/s",
         "value": U / step_s,
@@ -319,7 +328,8 @@ def run_b200(args):
         else None,
         "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "traffic_note": traffic_note,
                      "peak_source": FP64_PEAK_SRC + " (MEASURED_PEAKS.json has no FP64 entry)",
                      "kernel_ms_per_step": {k: v / steps for k, v in kms.items()},
                      "kernel_share": {k: v / max(sum(kms.values()), 1e-9)
