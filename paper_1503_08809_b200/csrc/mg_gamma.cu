@@ -835,7 +835,8 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     MG_CUDA(cudaMemsetAsync(P->sc->Z.p, 0, (size_t)nsplit * zsplit * sizeof(double), st));
     P->gamma.ensure((size_t)nm * nm);
 
-    static bool attr_done = false;
+    static bool attr_done_dev[64] = {false};  // function attributes are per device context
+    bool& attr_done = attr_done_dev[P->device & 63];
     const size_t smem_run = RunPipeP::smem_bytes;
     const XTile xt = choose_xtile(P2, pp);
     const size_t smem_x = xt == XTile::T120 ? XPipeT<CfgX120>::smem_bytes

@@ -314,3 +314,56 @@ class TestGamma2D:
             build_ptable(t, r, rule, legendre_table(16, rule), budget_bytes=1000)
         with pytest.raises(ValueError):
             build_ptable(t, r, rule, legendre_table(10, rule))
+
+
+class TestEdgeCases:
+    """Shapes the configs do not exercise: l_min > 2, odd Nx on a non-uniform grid (the
+    padded-x paths), a custom mode subset, p = 1, the single-triple domain (l_min = l_max)."""
+
+    def random_tables(self, lmin, lmax, p, nx, seed=0):
+        from paper_1503_08809_b200 import shifted_legendre
+        rng = np.random.default_rng(seed)
+        L = lmax - lmin + 1
+        q = shifted_legendre(p, lmin, lmax)
+        qt = rng.standard_normal((p, nx, L)) * 1e-3
+        C = rng.uniform(0.5, 2.0, L) * 1e-3
+        ells = np.arange(lmin, lmax + 1, dtype=np.float64)
+        v = (2.0 * ells + 1.0) ** (1.0 / 6.0)
+        r = np.cumsum(rng.uniform(0.5, 1.5, nx)) + 100.0
+        return BasisTables(q, qt, C, v, lmin, lmax), RadialGrid(r)
+
+    @pytest.mark.parametrize("lmin,lmax,p,nx,integ", [(3, 20, 4, 37, "spline"),
+                                                      (5, 41, 3, 33, "trap"),
+                                                      (2, 9, 1, 7, "hermite"),
+                                                      (2, 2, 2, 5, "trap"),
+                                                      (4, 4, 3, 9, "trap")])
+    def test_against_oracle(self, lmin, lmax, p, nx, integ):
+        from paper_1503_08809_b200 import default_mode_mapping
+        t, r = self.random_tables(lmin, lmax, p, nx)
+        m = default_mode_mapping(p)
+        got = gamma3d_matrix(t, m, r, integrator=integ).values
+        want = ref.gamma3d(t.q, t.q_tilde, t.C, t.v, x_weights(r.r, integ), m.entries, lmin,
+                           lmax)
+        if not np.any(want):
+            assert not np.any(got)
+        else:
+            assert frob_rel(got, want) < 1e-12
+
+    def test_custom_mode_subset(self):
+        t, r = self.random_tables(2, 30, 5, 41, seed=3)
+        entries = np.array([[0, 0, 0], [0, 2, 4], [1, 1, 3], [4, 4, 4], [0, 1, 2], [2, 3, 4]])
+        m = ModeMapping(entries, 5)
+        got = gamma3d_matrix(t, m, r).values
+        want = ref.gamma3d(t.q, t.q_tilde, t.C, t.v, x_weights(r.r), entries, 2, 30)
+        assert got.shape == (6, 6)
+        assert frob_rel(got, want) < 1e-12
+
+    def test_lmin_odd_flat_ranges(self):
+        from paper_1503_08809_b200 import default_mode_mapping
+        t, r = self.random_tables(3, 25, 3, 16, seed=5)
+        m = default_mode_mapping(3)
+        total = domain_count(3, 25)
+        for a, b in ((0, 1), (7, 93), (total - 5, total)):
+            got = gamma3d_matrix(t, m, r, domain=DomainRange(3, 25, a, b)).values
+            want = ref.gamma3d(t.q, t.q_tilde, t.C, t.v, x_weights(r.r), m.entries, 3, 25, a, b)
+            assert frob_rel(got, want) < 1e-12
