@@ -31,8 +31,18 @@
 
 namespace mg {
 
-constexpr int RUN_TN = 120;             // run-contraction N tile ((c', x) columns)
-constexpr int RUN_LDB = RUN_TN + 4;     // smem-identical row stride of WQB / A panels
+#ifndef MG_RUN_TILE96
+#define MG_RUN_TILE96 1
+#endif
+#if MG_RUN_TILE96
+constexpr int RUN_TN = 96;              // run-contraction N tile ((c', x) columns)
+constexpr int RUN_TM_ = 128;            // (row, c) slots per tile
+#else
+constexpr int RUN_TN = 120;
+constexpr int RUN_TM_ = 120;
+#endif
+constexpr int RUN_LDB = RUN_TN + 4;     // smem-identical row stride of WQB rows
+constexpr int RUN_LDA = RUN_TM_ + 4;    // smem-identical row stride of the A panels
 
 // ------------------------------------------------------------------------------------------
 // setup kernels
@@ -90,10 +100,16 @@ constexpr int X_LDK = X_BK + 4;  // x-blocked S/H row stride: [row][x/32][m][36]
 constexpr int PAIR_BK = 32, PAIR_ST = 3;
 using Cfg128 = TileCfg<2, 4, 8, 4>;   // 128 x 128, 8 warps, 64 accumulators per lane
 using CfgX120 = TileCfg<5, 3, 3, 5>;  // 120 x 120, 15 warps, 30 accumulators per lane
-using CfgRun = CfgX120;                // run contraction: 15 consumer warps + 1 producer
+// run contraction: 16 consumer warps (4 per SM sub-partition, so every DMMA unit has the same
+// number of warps to serve) + 1 producer warp; 128 packed (row,c) slots x 96 columns
+#if MG_RUN_TILE96
+using CfgRun = TileCfg<4, 4, 4, 3>;
+#else
+using CfgRun = CfgX120;
+#endif
 using PairPipe = Pipe<Cfg128, PAIR_BK, PAIR_ST, ASrc::KMajor, true, 0>;
 constexpr int RUN_TM = CfgRun::BM;     // (row, c) slots per run tile = A panel width
-static_assert(RUN_TN == CfgRun::BN && RUN_LDB == ld_kmajor(RUN_TM) &&
+static_assert(RUN_TN == CfgRun::BN && RUN_TM == RUN_TM_ && RUN_LDA == ld_kmajor(RUN_TM) &&
                   RUN_LDB == ld_kmajor(RUN_TN),
               "bulk-copied run tiles must match the shared-memory layout");
 constexpr int PANEL_THREADS = 256;
@@ -145,7 +161,7 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
                     val = z * q[(int64_t)c * L + (l1 - l_min)];
                 }
             }
-            out[(int64_t)(jc + jl) * RUN_LDB + slot] = val;
+            out[(int64_t)(jc + jl) * RUN_LDA + slot] = val;
         }
         __syncthreads();
     }
@@ -177,7 +193,7 @@ struct RunItems {
         return nk - (nk - 1) / RUN_BK * RUN_BK;
     }
     __device__ uint32_t stage_bytes(int, int) const {
-        return 2 * RUN_BK * RUN_LDB * (uint32_t)sizeof(double);
+        return RUN_BK * (RUN_LDA + RUN_LDB) * (uint32_t)sizeof(double);
     }
     __device__ void bulk_rows(int it, int kt, double* As, double* Bs, int lane,
                               uint64_t* bar) const {
@@ -185,8 +201,8 @@ struct RunItems {
         const int ti = it / NB, nb = it - ti * NB;
         const MgTile& t = tiles[ti];
         if (lane == 0) {
-            bulk_g2s(As, panel + poff[ti] + (int64_t)kt * RUN_BK * RUN_LDB,
-                     RUN_BK * RUN_LDB * sizeof(double), bar);
+            bulk_g2s(As, panel + poff[ti] + (int64_t)kt * RUN_BK * RUN_LDA,
+                     RUN_BK * RUN_LDA * sizeof(double), bar);
         } else {
             const int par = rows[t.row0].par;
             const double* w = WQB + (par ? wbase.y : wbase.x) +
@@ -297,97 +313,24 @@ k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __rest
     }
 }
 
+// Persistent x contraction: item it = (row r, M tile, N tile); tile shape per config.
 template <class Cfg>
-struct XPipeSel {
-    using type = Pipe<Cfg, X_BK, 3, ASrc::MMajor, false, 0>;
-};
-template <>
-struct XPipeSel<CfgX120> {
-    using type = PipeTMA<CfgX120, X_BK, 3, false, false>;
-};
-template <class Cfg>
-using XPipeT = typename XPipeSel<Cfg>::type;
-
-template <class Cfg>
-struct XProd {
-    const double* s;   // S + (r*XB*P2 + m0)*X_LDK     (x-blocked, block stride P2*X_LDK)
-    const double* h;   // H + (r*XB*pp + n0)*X_LDK     (x-blocked, block stride pp*X_LDK)
-    int64_t sblk, hblk;
-    int m_valid, n_valid, kv_last;
-    __device__ int kvalid_last() const { return kv_last; }
-    __device__ void issue(int kt, double* As, double* Bs, double*) const {
-        const double* sa = s + kt * sblk;
-        const double* hb = h + kt * hblk;
-        copy_mmajor<X_BK, Cfg::BM, Cfg::THREADS>(As, [&](int m) -> const double* {
-            return m < m_valid ? sa + (int64_t)m * X_LDK : nullptr;
-        }, X_BK);
-        copy_mmajor<X_BK, Cfg::BN, Cfg::THREADS>(Bs, [&](int m) -> const double* {
-            return m < n_valid ? hb + (int64_t)m * X_LDK : nullptr;
-        }, X_BK);
-    }
-    __device__ uint32_t stage_bytes(int) const {
-        return (m_valid + n_valid) * X_LDK * (uint32_t)sizeof(double);
-    }
-    // one bulk copy per operand: the x-blocked global layout equals the smem tile layout
-    __device__ void bulk_rows(int kt, double* As, double* Bs, int lane, uint64_t* bar) const {
-        if (lane == 0)
-            bulk_g2s(As, s + kt * sblk, m_valid * X_LDK * sizeof(double), bar);
-        else if (lane == 1)
-            bulk_g2s(Bs, h + kt * hblk, n_valid * X_LDK * sizeof(double), bar);
-    }
-};
-
-template <class Cfg>
-__global__ void __launch_bounds__(XPipeT<Cfg>::THREADS, 1)
-k_x_contract(const double* __restrict__ S, const double* __restrict__ H, int row_b1,
-             int row_b3, int p, int P2, int Nx, int NxP, double* __restrict__ G) {
-    extern __shared__ __align__(16) double smem[];
-    const int r = blockIdx.z;  // row within the K1/K2 batch
-    const int m0 = blockIdx.y * Cfg::BM, n0 = blockIdx.x * Cfg::BN;
-    const int pp = p * p;
-    XProd<Cfg> pr;
-    const int XB = NxP / X_BK;
-    pr.s = S + ((int64_t)r * XB * P2 + m0) * X_LDK;
-    pr.h = H + ((int64_t)r * XB * pp + n0) * X_LDK;
-    pr.sblk = (int64_t)P2 * X_LDK;
-    pr.hblk = (int64_t)pp * X_LDK;
-    pr.m_valid = min(Cfg::BM, P2 - m0);
-    pr.n_valid = min(Cfg::BN, pp - n0);
-    pr.kv_last = Nx - (NxP / X_BK - 1) * X_BK;
-    Acc<Cfg> acc;
-    if constexpr (std::is_same_v<XPipeT<Cfg>, Pipe<Cfg, X_BK, 3, ASrc::MMajor, false, 0>>) {
-        XPipeT<Cfg>::run(NxP / X_BK, pr, smem, acc);
-    } else {
-        if (!XPipeT<Cfg>::run(NxP / X_BK, pr, smem, acc)) return;  // producer warp
-    }
-    double* Gr = G + (int64_t)(row_b1 + r - row_b3) * pp * P2;
-    acc_foreach_pair<Cfg>(acc, [&](int m, int n, double v0, double v1) {
-        int prr = m0 + m, cc = n0 + n;
-        if (prr < P2) {
-            if (cc < pp) Gr[(int64_t)cc * P2 + prr] = v0;
-            if (cc + 1 < pp) Gr[(int64_t)(cc + 1) * P2 + prr] = v1;
-        }
-    });
-}
-
-// Persistent x contraction for the 120 x 120 tile: item it = (row r, M tile, N tile).
 struct XItems {
     const double* S;
     const double* H;
-    int P2, pp, XB, MT, NT;
+    int P2, pp, XB, MT, NT, kv_last;
     __device__ void decode(int it, int& r, int& mt, int& nt) const {
         nt = it % NT;
         mt = (it / NT) % MT;
         r = it / (NT * MT);
     }
     __device__ int ktiles(int) const { return XB; }
-    int kv_last;
     __device__ int kvalid_last(int) const { return kv_last; }
     __device__ uint32_t stage_bytes(int it, int) const {
         int r, mt, nt;
         decode(it, r, mt, nt);
-        const int mv = min(CfgX120::BM, P2 - mt * CfgX120::BM);
-        const int nv = min(CfgX120::BN, pp - nt * CfgX120::BN);
+        const int mv = min(Cfg::BM, P2 - mt * Cfg::BM);
+        const int nv = min(Cfg::BN, pp - nt * Cfg::BN);
         return (mv + nv) * X_LDK * (uint32_t)sizeof(double);
     }
     __device__ void bulk_rows(int it, int kt, double* As, double* Bs, int lane,
@@ -396,33 +339,35 @@ struct XItems {
         int r, mt, nt;
         decode(it, r, mt, nt);
         if (lane == 0) {
-            const int mv = min(CfgX120::BM, P2 - mt * CfgX120::BM);
-            bulk_g2s(As, S + (((int64_t)r * XB + kt) * P2 + mt * CfgX120::BM) * X_LDK,
+            const int mv = min(Cfg::BM, P2 - mt * Cfg::BM);
+            bulk_g2s(As, S + (((int64_t)r * XB + kt) * P2 + mt * Cfg::BM) * X_LDK,
                      mv * X_LDK * sizeof(double), bar);
         } else {
-            const int nv = min(CfgX120::BN, pp - nt * CfgX120::BN);
-            bulk_g2s(Bs, H + (((int64_t)r * XB + kt) * pp + nt * CfgX120::BN) * X_LDK,
+            const int nv = min(Cfg::BN, pp - nt * Cfg::BN);
+            bulk_g2s(Bs, H + (((int64_t)r * XB + kt) * pp + nt * Cfg::BN) * X_LDK,
                      nv * X_LDK * sizeof(double), bar);
         }
     }
 };
-using XPipeP = PipeTMAPersistent<CfgX120, X_BK, 3, false, false>;
+template <class Cfg>
+using XPipeP = PipeTMAPersistent<Cfg, X_BK, 3, false, false>;
 
-__global__ void __launch_bounds__(XPipeP::THREADS, 1)
+template <class Cfg>
+__global__ void __launch_bounds__(XPipeP<Cfg>::THREADS, 1)
 k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int nrows,
                int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* __restrict__ G) {
     extern __shared__ __align__(16) double smem[];
     const int pp = p * p;
-    XItems items{S, H, P2, pp, NxP / X_BK, (P2 + CfgX120::BM - 1) / CfgX120::BM,
-                 (pp + CfgX120::BN - 1) / CfgX120::BN, 0};
+    XItems<Cfg> items{S, H, P2, pp, NxP / X_BK, (P2 + Cfg::BM - 1) / Cfg::BM,
+                      (pp + Cfg::BN - 1) / Cfg::BN, 0};
     items.kv_last = Nx - (items.XB - 1) * X_BK;
     const int nitems = nrows * items.MT * items.NT;
-    XPipeP::run(blockIdx.x, gridDim.x, nitems, items, [&](int it, const Acc<CfgX120>& acc) {
+    XPipeP<Cfg>::run(blockIdx.x, gridDim.x, nitems, items, [&](int it, const Acc<Cfg>& acc) {
         int r, mt, nt;
         items.decode(it, r, mt, nt);
-        const int m0 = mt * CfgX120::BM, n0 = nt * CfgX120::BN;
+        const int m0 = mt * Cfg::BM, n0 = nt * Cfg::BN;
         double* Gr = G + (int64_t)(row_b1 + r - row_b3) * pp * P2;
-        acc_foreach_pair<CfgX120>(acc, [&](int m, int n, double v0, double v1) {
+        acc_foreach_pair<Cfg>(acc, [&](int m, int n, double v0, double v1) {
             const int prr = m0 + m, cc = n0 + n;
             if (prr < P2) {
                 if (cc < pp) Gr[(int64_t)cc * P2 + prr] = v0;
@@ -432,13 +377,21 @@ k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int n
     }, smem);
 }
 
-// Tile choice for the x contraction: the config with the least padded M x N area.
-enum class XTile { T128, T120 };
+using CfgX160 = TileCfg<4, 4, 5, 3>;   // 160 x 96, 16 consumer warps (p = 30)
+using CfgX128 = TileCfg<2, 4, 8, 4>;   // 128 x 128, 8 consumer warps (p = 22)
+
+// Tile choice for the x contraction: padded-area efficiency of M = p(p+1)/2, N = p^2, times
+// the sub-partition balance of the consumer warps (15 warps leave one of the four SMSPs with
+// three: at most 15/16 of the DMMA units busy).
+enum class XTile { T120, T160, T128 };
 static XTile choose_xtile(int P2, int pp) {
-    auto area = [&](int bm, int bn) {
-        return (double)ceil_div(P2, bm) * bm * ceil_div(pp, bn) * bn;
+    auto eff = [&](int bm, int bn, double bal) {
+        return bal * (double)P2 * pp / ((double)ceil_div(P2, bm) * bm * ceil_div(pp, bn) * bn);
     };
-    return area(120, 120) < area(128, 128) ? XTile::T120 : XTile::T128;
+    const double e120 = eff(120, 120, 15.0 / 16.0), e160 = eff(160, 96, 1.0),
+                 e128 = eff(128, 128, 1.0);
+    if (e120 >= e160 && e120 >= e128) return XTile::T120;
+    return e160 >= e128 ? XTile::T160 : XTile::T128;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -761,7 +714,7 @@ static void prepare_batches(mg_plan* P, const std::vector<MgRow>& hrows,
                 max_tile_rows = std::max(max_tile_rows, t.nrows);
                 tiles.push_back(t);
                 poff.push_back(off);
-                off += round_up(t.jhi - t.jlo + 1, RUN_BK) * RUN_LDB;
+                off += round_up(t.jhi - t.jlo + 1, RUN_BK) * RUN_LDA;
             }
             g0 = g1;
         }
@@ -839,17 +792,22 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     bool& attr_done = attr_done_dev[P->device & 63];
     const size_t smem_run = RunPipeP::smem_bytes;
     const XTile xt = choose_xtile(P2, pp);
-    const size_t smem_x = xt == XTile::T120 ? XPipeT<CfgX120>::smem_bytes
-                                            : XPipeT<Cfg128>::smem_bytes;
+    const size_t smem_x = xt == XTile::T120   ? XPipeP<CfgX120>::smem_bytes
+                          : xt == XTile::T160 ? XPipeP<CfgX160>::smem_bytes
+                                              : XPipeP<CfgX128>::smem_bytes;
     const size_t smem_pair = PairPipe::smem_bytes;
     if (!attr_done) {
         MG_CUDA(cudaFuncSetAttribute(k_run_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_run));
-        MG_CUDA(cudaFuncSetAttribute(k_x_contract_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)XPipeP::smem_bytes));
-        MG_CUDA(cudaFuncSetAttribute(k_x_contract<Cfg128>,
+        MG_CUDA(cudaFuncSetAttribute(k_x_contract_p<CfgX120>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)XPipeT<Cfg128>::smem_bytes));
+                                     (int)XPipeP<CfgX120>::smem_bytes));
+        MG_CUDA(cudaFuncSetAttribute(k_x_contract_p<CfgX160>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)XPipeP<CfgX160>::smem_bytes));
+        MG_CUDA(cudaFuncSetAttribute(k_x_contract_p<CfgX128>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)XPipeP<CfgX128>::smem_bytes));
         MG_CUDA(cudaFuncSetAttribute(k_pair_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_pair));
         attr_done = true;
@@ -901,12 +859,14 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             MG_LAUNCHED();
             prof_mark(P, 2, st);
             if (xt == XTile::T120) {
-                k_x_contract_p<<<num_sms, XPipeP::THREADS, XPipeP::smem_bytes, st>>>(
+                k_x_contract_p<CfgX120><<<num_sms, XPipeP<CfgX120>::THREADS, smem_x, st>>>(
+                    P->sc->S.p, P->sc->H.p, nb, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
+            } else if (xt == XTile::T160) {
+                k_x_contract_p<CfgX160><<<num_sms, XPipeP<CfgX160>::THREADS, smem_x, st>>>(
                     P->sc->S.p, P->sc->H.p, nb, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
             } else {
-                dim3 g2(ceil_div(pp, Cfg128::BN), ceil_div(P2, Cfg128::BM), nb);
-                k_x_contract<Cfg128><<<g2, XPipeT<Cfg128>::THREADS, smem_x, st>>>(
-                    P->sc->S.p, P->sc->H.p, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
+                k_x_contract_p<CfgX128><<<num_sms, XPipeP<CfgX128>::THREADS, smem_x, st>>>(
+                    P->sc->S.p, P->sc->H.p, nb, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
             }
             MG_LAUNCHED();
             launches += 4 + (dt1 ? 1 : 0);
