@@ -191,12 +191,17 @@ def run_b200(args):
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     gloo = args.dist_backend == "gloo"
+    backend_note = None
     if world > 1:
         import torch.distributed as dist
+        if not gloo:
+            try:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            except Exception as exc:  # keep the run alive: the exchange is one n x n Γ
+                backend_note = f"nccl init failed ({type(exc).__name__}); Γ exchanged over gloo"
+                gloo = True
         if gloo:
             dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = CONFIGS[args.config]
     hi = host_inputs(spec)
     T, U, nmodes = total_updates(spec)
@@ -313,7 +318,8 @@ def run_b200(args):
         "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config shapes; q̃ built on-device from "
                 "Bessel/transfer inputs)",
-        "dist_backend": args.dist_backend if world > 1 else None,
+        "dist_backend": (("gloo" if gloo else "nccl") if world > 1 else None),
+        "dist_note": backend_note,
         "config": {"workload": f"separable Γ, BASELINE config {args.config[1:]}: "
                                f"l_max={spec.l_max}, p={spec.p} -> {nmodes} modes, "
                                f"Nx={spec.n_x}, Nk={spec.n_k}, T={T} ordered triples",
