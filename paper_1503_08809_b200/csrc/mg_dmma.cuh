@@ -203,8 +203,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(
-        smem_u32(bar)));
+        smem_u32(bar)) : "memory");
 }
+// Blocking wait for the phase with the given parity.  The "memory" clobber keeps the compiler
+// from hoisting shared-memory reads of the stage above the wait.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, int parity) {
     asm volatile(
         "{\n"
@@ -213,7 +215,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, int parity) {
         " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         " @!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity));
+        "r"(parity) : "memory");
+}
+// Non-blocking probe of the same phase (1 = complete).  Issued well before the data is
+// needed, its result is consumed only at the stage boundary, so the probe's latency overlaps
+// the DMMAs of the current stage instead of stalling every consumer warp at once.
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, int parity) {
+    uint32_t r;
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n"
+        "}\n" : "=r"(r) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return r;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -358,9 +373,22 @@ struct PipeTMAPersistent {
             return;
         }
         // ------------------------------------------------------------- consumer warps
+        // The fragments of a stage's first k4 step are loaded while the previous stage's last
+        // k4 step is still in the DMMA pipe, and the stage's barrier is probed one stage
+        // early, so crossing a stage boundary costs no exposed barrier or LDS latency.
+        static_assert((BK / 4) % 2 == 0, "cross-stage fragment prefetch needs an even k4 count");
         const int g4 = lane >> 2, t = lane & 3;
         const int wm = (warp / Cfg::WARPS_N) * (8 * FM), wn = (warp % Cfg::WARPS_N) * (8 * FN);
         Acc<Cfg> acc;
+        double a[2][FM], b[2][FN];
+        auto load_frags = [&](int buf, const double* As, const double* Bs, int k) {
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
+                a[buf][mi] = frag_ld<AK, Cfg::BM, BK>(As, k, wm + mi * 8 + g4);
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni)
+                b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g4);
+        };
         int g = 0;
         for (int it = first; it < nitems; it += stride) {
 #pragma unroll
@@ -369,27 +397,31 @@ struct PipeTMAPersistent {
                 for (int ni = 0; ni < FN; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
             const int kts = prod.ktiles(it);
             const int kvl = prod.kvalid_last(it);
-            for (int kt = 0; kt < kts; ++kt, ++g) {
+            {
                 const int s = g % STAGES;
                 mbar_wait(full + s, (g / STAGES) & 1);
+                load_frags(0, smem + s * SS, smem + s * SS + SA, t);
+            }
+            for (int kt = 0; kt < kts; ++kt, ++g) {
+                const int s = g % STAGES, s2 = (g + 1) % STAGES;
+                const int ph2 = ((g + 1) / STAGES) & 1;
                 const double* As = smem + s * SS;
                 const double* Bs = As + SA;
-                double a[2][FM], b[2][FN];
-                auto load_frags = [&](int buf, int k) {
-#pragma unroll
-                    for (int mi = 0; mi < FM; ++mi)
-                        a[buf][mi] = frag_ld<AK, Cfg::BM, BK>(As, k, wm + mi * 8 + g4);
-#pragma unroll
-                    for (int ni = 0; ni < FN; ++ni)
-                        b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g4);
-                };
-                const int nks = kt + 1 < kts ? BK / 4 : (kvl + 3) / 4;
-                load_frags(0, t);
+                const double* As2 = smem + s2 * SS;
+                const double* Bs2 = As2 + SA;
+                const bool more = kt + 1 < kts;
+                const int nks = more ? BK / 4 : (kvl + 3) / 4;
+                uint32_t ready = more ? mbar_test(full + s2, ph2) : 1u;
 #pragma unroll
                 for (int ks = 0; ks < BK / 4; ++ks) {
                     if (ks < nks) {
                         const int cur = ks & 1;
-                        if (ks + 1 < BK / 4) load_frags(cur ^ 1, (ks + 1) * 4 + t);
+                        if (ks + 1 < BK / 4) {
+                            load_frags(cur ^ 1, As, Bs, (ks + 1) * 4 + t);
+                        } else if (more) {
+                            if (!ready) mbar_wait(full + s2, ph2);
+                            load_frags(cur ^ 1, As2, Bs2, t);
+                        }
 #pragma unroll
                         for (int mi = 0; mi < FM; ++mi)
 #pragma unroll

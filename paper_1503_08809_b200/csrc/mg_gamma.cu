@@ -94,7 +94,11 @@ __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t*
 // K1a: A panels of the run contraction, one per M-tile, k-major [jl][slot]:
 //   panel[jl][slot=(r,c)] = zm(l1(j), l2_r, l3_r) q_c(l1(j))  (0 outside row r's window)
 // ------------------------------------------------------------------------------------------
-constexpr int RUN_BK = 16, RUN_ST = 6;
+#ifndef MG_RUN_BK
+#define MG_RUN_BK 32
+#define MG_RUN_ST 3
+#endif
+constexpr int RUN_BK = MG_RUN_BK, RUN_ST = MG_RUN_ST;
 constexpr int X_BK = 32;
 constexpr int X_LDK = X_BK + 4;  // x-blocked S/H row stride: [row][x/32][m][36], smem-identical
 constexpr int PAIR_BK = 32, PAIR_ST = 3;
