@@ -130,8 +130,9 @@ int mg_plan_stats(mg_plan* plan, double* flops_rowcontract, double* flops_xcontr
                   double* flops_pairs, int64_t* launches);
 /* Per-kernel-family timing with CUDA events on the launching stream (bench roofline):
  * after mg_plan_set_profile(plan, 1), every execute accumulates milliseconds into
- * ms[6] = {operand builds (A panels, pair products), run contraction, x contraction,
- *          R gather, pair contraction, final}. */
+ * ms[7] = {exposed wait of the contractions for their operands, run contraction,
+ *          x contraction, R gather, pair contraction, final,
+ *          operand kernels (A panels, pair products) on the side stream, overlapped}. */
 int mg_plan_set_profile(mg_plan* plan, int on);
 int mg_plan_kernel_ms(mg_plan* plan, double* ms);
 void mg_plan_destroy(mg_plan* plan);

@@ -247,6 +247,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
                  ::"r"(smem_u32(bar)), "r"(bytes));
 }
+// Raise the transaction count of the current phase without arriving (the arrivals come
+// later, from the lanes that also write part of the stage with ordinary shared stores).
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
@@ -351,7 +357,7 @@ struct PipeTMAPersistent {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         if (threadIdx.x == 0) {
             for (int s = 0; s < STAGES; ++s) {
-                mbar_init(full + s, 1);
+                mbar_init(full + s, Prod::kComputeA ? 32 : 1);
                 mbar_init(empty + s, WARPS);
             }
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
@@ -364,10 +370,21 @@ struct PipeTMAPersistent {
                 for (int kt = 0; kt < kts; ++kt, ++g) {
                     const int s = g % STAGES;
                     if (g >= STAGES) mbar_wait(empty + s, ((g / STAGES) - 1) & 1);
-                    if (lane == 0) mbar_arrive_expect_tx(full + s, prod.stage_bytes(it, kt));
-                    __syncwarp();
                     double* st = smem + s * SS;
-                    prod.bulk_rows(it, kt, st, st + SA, lane, full + s);
+                    if constexpr (Prod::kComputeA) {
+                        // B by bulk copy; A computed by the 32 lanes with shared stores, each
+                        // lane's arrive releasing its own stores to the consumers
+                        if (lane == 0) {
+                            mbar_expect_tx(full + s, prod.stage_bytes(it, kt));
+                            prod.bulk_b(it, kt, st + SA, full + s);
+                        }
+                        prod.compute_a(it, kt, st, lane);
+                        mbar_arrive(full + s);
+                    } else {
+                        if (lane == 0) mbar_arrive_expect_tx(full + s, prod.stage_bytes(it, kt));
+                        __syncwarp();
+                        prod.bulk_rows(it, kt, st, st + SA, lane, full + s);
+                    }
                 }
             }
             return;

@@ -94,6 +94,9 @@ __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t*
 // K1a: A panels of the run contraction, one per M-tile, k-major [jl][slot]:
 //   panel[jl][slot=(r,c)] = zm(l1(j), l2_r, l3_r) q_c(l1(j))  (0 outside row r's window)
 // ------------------------------------------------------------------------------------------
+#ifndef MG_SIDE  // operand kernels on the side stream: 0 none, 1 pair products, 2 + panels
+#define MG_SIDE 1
+#endif
 #ifndef MG_RUN_BK
 #define MG_RUN_BK 32
 #define MG_RUN_ST 3
@@ -101,8 +104,6 @@ __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t*
 constexpr int RUN_BK = MG_RUN_BK, RUN_ST = MG_RUN_ST;
 constexpr int X_BK = 32;
 constexpr int X_LDK = X_BK + 4;  // x-blocked S/H row stride: [row][x/32][m][36], smem-identical
-constexpr int PAIR_BK = 32, PAIR_ST = 3;
-using Cfg128 = TileCfg<2, 4, 8, 4>;   // 128 x 128, 8 warps, 64 accumulators per lane
 using CfgX120 = TileCfg<5, 3, 3, 5>;  // 120 x 120, 15 warps, 30 accumulators per lane
 // run contraction: 16 consumer warps (4 per SM sub-partition, so every DMMA unit has the same
 // number of warps to serve) + 1 producer warp; 128 packed (row,c) slots x 96 columns
@@ -111,7 +112,6 @@ using CfgRun = TileCfg<4, 4, 4, 3>;
 #else
 using CfgRun = CfgX120;
 #endif
-using PairPipe = Pipe<Cfg128, PAIR_BK, PAIR_ST, ASrc::KMajor, true, 0>;
 constexpr int RUN_TM = CfgRun::BM;     // (row, c) slots per run tile = A panel width
 static_assert(RUN_TN == CfgRun::BN && RUN_TM == RUN_TM_ && RUN_LDA == ld_kmajor(RUN_TM) &&
                   RUN_LDB == ld_kmajor(RUN_TN),
@@ -128,12 +128,14 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
              const double* __restrict__ C, const double* __restrict__ v,
              const double* __restrict__ lf, const double* __restrict__ fl, int mode,
              double* __restrict__ panel) {
-    extern __shared__ double zs[];  // [nrows][PANEL_JC]: zm of (row, j) for the current chunk
+    extern __shared__ double zs[];  // [nrows][PANEL_JC]: zm of (row, j) for this chunk
     const MgTile tl = tiles[blockIdx.x];
     const int kt = (tl.jhi - tl.jlo + RUN_BK) / RUN_BK * RUN_BK;
     double* out = panel + poff[blockIdx.x];
     const int par = rows[tl.row0].par;
-    for (int jc = 0; jc < kt; jc += PANEL_JC) {
+    {  // one block per (tile, chunk of PANEL_JC j values)
+        const int jc = blockIdx.y * PANEL_JC;
+        if (jc >= kt) return;
         // 1) each (row, j) weight once
         for (int e = threadIdx.x; e < tl.nrows * PANEL_JC; e += PANEL_THREADS) {
             const int rr = e / PANEL_JC, jl = e % PANEL_JC;
@@ -179,6 +181,7 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
 // Persistent run contraction: item it = tile * NB + column block; items are strided over the
 // CTAs (one per SM).  The producer warp streams the next item while consumers write H.
 struct RunItems {
+    static constexpr bool kComputeA = false;
     const MgTile* tiles;
     const int64_t* poff;
     const double* panel;
@@ -288,8 +291,11 @@ __device__ __forceinline__ int pair_idx(int a, int b) {  // a <= b
     return b * (b + 1) / 2 + a;
 }
 
-constexpr int PP_CHUNK = 8;  // pairs per block of the pair-product kernel
+constexpr int PP_CHUNK = 16;  // pairs per block of the pair-product kernel
 
+// K2a: S[r][ab][x] = q̃_a(x,l2)q̃_b(x,l3) + q̃_b(x,l2)q̃_a(x,l3) in the x-blocked layout of the
+// x contraction.  One block per (row, chunk of 16 pairs); a thread owns an x pair (double2) and
+// walks the chunk b-major: q̃_b(l2), q̃_b(l3) stay in registers while four a's are loaded at once.
 __global__ void __launch_bounds__(256)
 k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __restrict__ QT,
                 int p, int P2, int NxP, int l_min, double* __restrict__ S) {
@@ -299,27 +305,45 @@ k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __rest
     const double2* q3 = reinterpret_cast<const double2*>(QT + (int64_t)(rw.l3 - l_min) * p * NxP);
     double* out = S + (int64_t)r * P2 * (NxP / X_BK) * X_LDK;
     const int nx2 = NxP / 2;
-    int pr = blockIdx.x * PP_CHUNK, a, b;
-    pair_of(pr, a, b);
-    for (int i = 0; i < PP_CHUNK && pr < P2; ++i, ++pr) {
-        const double2* a2 = q2 + a * nx2;
-        const double2* b2 = q2 + b * nx2;
-        const double2* a3 = q3 + a * nx2;
-        const double2* b3 = q3 + b * nx2;
-        for (int x = threadIdx.x; x < nx2; x += blockDim.x) {
-            double2 u = a2[x], w = b3[x], y = b2[x], z = a3[x];
-            const int xx = 2 * x;
-            *reinterpret_cast<double2*>(out + ((int64_t)(xx / X_BK) * P2 + pr) * X_LDK +
-                                        (xx & (X_BK - 1))) =
-                make_double2(u.x * w.x + y.x * z.x, u.y * w.y + y.y * z.y);
+    const int pr0 = blockIdx.x * PP_CHUNK, pr1 = min(pr0 + PP_CHUNK, P2);
+    int a0, b0;
+    pair_of(pr0, a0, b0);
+    for (int x = threadIdx.x; x < nx2; x += blockDim.x) {
+        const int xx = 2 * x;
+        double* o = out + (int64_t)(xx / X_BK) * P2 * X_LDK + (xx & (X_BK - 1));
+        int a = a0, b = b0, pr = pr0;
+        while (pr < pr1) {
+            const double2 ub = __ldg(q2 + b * nx2 + x), wb = __ldg(q3 + b * nx2 + x);
+            const int na = min(b + 1 - a, pr1 - pr);  // pairs (a .. a+na-1, b)
+            int i = 0;
+            for (; i + 4 <= na; i += 4) {
+                double2 u[4], w[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    u[k] = __ldg(q2 + (a + i + k) * nx2 + x);
+                    w[k] = __ldg(q3 + (a + i + k) * nx2 + x);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    *reinterpret_cast<double2*>(o + (int64_t)(pr + i + k) * X_LDK) =
+                        make_double2(u[k].x * wb.x + ub.x * w[k].x, u[k].y * wb.y + ub.y * w[k].y);
+            }
+            for (; i < na; ++i) {
+                const double2 u = __ldg(q2 + (a + i) * nx2 + x), w = __ldg(q3 + (a + i) * nx2 + x);
+                *reinterpret_cast<double2*>(o + (int64_t)(pr + i) * X_LDK) =
+                    make_double2(u.x * wb.x + ub.x * w.x, u.y * wb.y + ub.y * w.y);
+            }
+            pr += na;
+            a = 0;
+            ++b;
         }
-        if (++a > b) { ++b; a = 0; }  // next pair in b-major order
     }
 }
 
 // Persistent x contraction: item it = (row r, M tile, N tile); tile shape per config.
 template <class Cfg>
 struct XItems {
+    static constexpr bool kComputeA = false;
     const double* S;
     const double* H;
     int P2, pp, XB, MT, NT, kv_last;
@@ -404,33 +428,43 @@ static XTile choose_xtile(int P2, int pp) {
 // ------------------------------------------------------------------------------------------
 __global__ void k_gather(const MgRow* __restrict__ rows, const double* __restrict__ G,
                          const int* __restrict__ modes, const double* __restrict__ q, int L,
-                         int l_min, int p, int P2, int nm, int64_t ldr, int ldq,
-                         double* __restrict__ R, double* __restrict__ Sq) {
+                         int l_min, int p, int P2, int nm, int n3, int64_t kp,
+                         double* __restrict__ RB, double* __restrict__ SqB) {
+    // Blocked, smem-identical layouts of the pair contraction's operands (one bulk copy per
+    // stage): RB[nt][r][RUN_LDB] (column c = nt*RUN_TN + cn), SqB[mt][r][RUN_LDA] (pair
+    // pr = mt*RUN_TM + m).  Rows r in [n3, gridDim.y) are the zero K-padding of the last tile.
     const int r = blockIdx.y;
+    const bool live = r < n3;
     const int pp = p * p;
     const double* Gr = G + (int64_t)r * pp * P2;
     const int ncols = p * nm;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < ncols;
          idx += gridDim.x * blockDim.x) {
-        int c = idx / nm, np = idx - c * nm;
-        int a = modes[3 * np], b = modes[3 * np + 1], d = modes[3 * np + 2];
-        int cp = c * p;
-        R[(int64_t)r * ldr + idx] = Gr[(int64_t)(cp + d) * P2 + pair_idx(a, b)] +
-                                    Gr[(int64_t)(cp + b) * P2 + pair_idx(a, d)] +
-                                    Gr[(int64_t)(cp + a) * P2 + pair_idx(b, d)];
+        double val = 0.0;
+        if (live) {
+            int c = idx / nm, np = idx - c * nm;
+            int a = modes[3 * np], b = modes[3 * np + 1], d = modes[3 * np + 2];
+            int cp = c * p;
+            val = Gr[(int64_t)(cp + d) * P2 + pair_idx(a, b)] +
+                  Gr[(int64_t)(cp + b) * P2 + pair_idx(a, d)] +
+                  Gr[(int64_t)(cp + a) * P2 + pair_idx(b, d)];
+        }
+        const int nt = idx / RUN_TN, cn = idx - nt * RUN_TN;
+        RB[((int64_t)nt * kp + r) * RUN_LDB + cn] = val;
     }
     if (blockIdx.x == 0) {
-        const MgRow w = rows[r];
-        for (int pr = threadIdx.x; pr < ldq; pr += blockDim.x) {
+        const MgRow w = rows[live ? r : 0];
+        for (int pr = threadIdx.x; pr < P2; pr += blockDim.x) {
             double s = 0.0;
-            if (pr < P2) {
+            if (live) {
                 int a, b;
                 pair_of(pr, a, b);
                 const double* qa = q + (int64_t)a * L - l_min;
                 const double* qb = q + (int64_t)b * L - l_min;
                 s = qa[w.l2] * qb[w.l3] + qb[w.l2] * qa[w.l3];
             }
-            Sq[(int64_t)r * ldq + pr] = s;
+            const int mt = pr / RUN_TM, m = pr - mt * RUN_TM;
+            SqB[((int64_t)mt * kp + r) * RUN_LDA + m] = s;
         }
     }
 }
@@ -438,54 +472,71 @@ __global__ void k_gather(const MgRow* __restrict__ rows, const double* __restric
 // ------------------------------------------------------------------------------------------
 // K3: pair contraction over rows  Z_s[ab][(c,n')] += Σ_{r in split s} Sq[r][ab] R[r][(c,n')]
 // ------------------------------------------------------------------------------------------
-struct PairProd {
-    const double* sq;  // Sq + r0*ldq + m0
-    const double* rr;  // R + r0*ldr + n0
-    int ldq;
-    int64_t ldr;
-    int nr, m_valid, n_valid;
-    __device__ int kvalid_last() const { return nr - (nr - 1) / PAIR_BK * PAIR_BK; }
-    __device__ void issue(int kt, double* As, double* Bs, double*) const {
-        copy_kmajor<PAIR_BK, 128, 256>(As, [&](int k) -> const double* {
-            int r = kt * PAIR_BK + k;
-            return r < nr ? sq + (int64_t)r * ldq : nullptr;
-        }, m_valid);
-        copy_kmajor<PAIR_BK, 128, 256>(Bs, [&](int k) -> const double* {
-            int r = kt * PAIR_BK + k;
-            return r < nr ? rr + (int64_t)r * ldr : nullptr;
-        }, n_valid);
+// Persistent pair contraction: item it = (split s, M tile, N tile) over the 128 x 96 run
+// tile and pipeline; stages are one bulk copy of SqB and one of RB.
+struct PairItems {
+    static constexpr bool kComputeA = false;
+    const double* SqB;
+    const double* RB;
+    int64_t kp;
+    int n3, per, MT, NT;
+    __device__ void decode(int it, int& s, int& mt, int& nt) const {
+        nt = it % NT;
+        mt = (it / NT) % MT;
+        s = it / (NT * MT);
+    }
+    __device__ int rows_of(int s) const { return min(per, n3 - s * per); }
+    __device__ int ktiles(int it) const {
+        int s, mt, nt;
+        decode(it, s, mt, nt);
+        return (rows_of(s) + RUN_BK - 1) / RUN_BK;
+    }
+    __device__ int kvalid_last(int it) const {
+        int s, mt, nt;
+        decode(it, s, mt, nt);
+        const int nr = rows_of(s);
+        return nr - (nr - 1) / RUN_BK * RUN_BK;
+    }
+    __device__ uint32_t stage_bytes(int, int) const {
+        return RUN_BK * (RUN_LDA + RUN_LDB) * (uint32_t)sizeof(double);
+    }
+    __device__ void bulk_rows(int it, int kt, double* As, double* Bs, int lane,
+                              uint64_t* bar) const {
+        if (lane > 1) return;
+        int s, mt, nt;
+        decode(it, s, mt, nt);
+        const int64_t r = (int64_t)s * per + kt * RUN_BK;
+        if (lane == 0)
+            bulk_g2s(As, SqB + ((int64_t)mt * kp + r) * RUN_LDA,
+                     RUN_BK * RUN_LDA * sizeof(double), bar);
+        else
+            bulk_g2s(Bs, RB + ((int64_t)nt * kp + r) * RUN_LDB,
+                     RUN_BK * RUN_LDB * sizeof(double), bar);
     }
 };
 
-__global__ void __launch_bounds__(256, 1)
-k_pair_contract(const double* __restrict__ Sq, int ldq, const double* __restrict__ R,
-                int64_t ldr, int nrows, int per_split, int P2, int ncols, int64_t zsplit,
+__global__ void __launch_bounds__(RunPipeP::THREADS, 1)
+k_pair_contract(const double* __restrict__ SqB, const double* __restrict__ RB, int64_t kp,
+                int n3, int per, int nsplit, int P2, int ncols, int64_t zsplit,
                 double* __restrict__ Z) {
     extern __shared__ __align__(16) double smem[];
-    const int m0 = blockIdx.y * Cfg128::BM, n0 = blockIdx.x * Cfg128::BN;
-    const int s = blockIdx.z;
-    const int r0 = s * per_split;
-    const int nr = min(per_split, nrows - r0);
-    if (nr <= 0) return;
-    PairProd pr;
-    pr.sq = Sq + (int64_t)r0 * ldq + m0;
-    pr.rr = R + (int64_t)r0 * ldr + n0;
-    pr.ldq = ldq;
-    pr.ldr = ldr;
-    pr.nr = nr;
-    pr.m_valid = min(Cfg128::BM, P2 - m0);
-    pr.n_valid = min(Cfg128::BN, ncols - n0);
-    Acc<Cfg128> acc;
-    PairPipe::run((nr + PAIR_BK - 1) / PAIR_BK, pr, smem, acc);
-    double* Zs = Z + s * zsplit;
-    acc_foreach_pair<Cfg128>(acc, [&](int m, int n, double v0, double v1) {
-        int prr = m0 + m, c = n0 + n;
-        if (prr < P2) {
-            double* z = Zs + (int64_t)prr * ncols;
-            if (c < ncols) z[c] += v0;
-            if (c + 1 < ncols) z[c + 1] += v1;
-        }
-    });
+    PairItems items{SqB, RB, kp, n3, per, (P2 + RUN_TM - 1) / RUN_TM,
+                    (ncols + RUN_TN - 1) / RUN_TN};
+    const int nitems = nsplit * items.MT * items.NT;
+    RunPipeP::run(blockIdx.x, gridDim.x, nitems, items, [&](int it, const Acc<CfgRun>& acc) {
+        int s, mt, nt;
+        items.decode(it, s, mt, nt);
+        double* Zs = Z + s * zsplit;
+        const int m0 = mt * RUN_TM, n0 = nt * RUN_TN;
+        acc_foreach_pair<CfgRun>(acc, [&](int m, int n, double v0, double v1) {
+            const int prr = m0 + m, c = n0 + n;
+            if (prr < P2) {
+                double* z = Zs + (int64_t)prr * ncols;
+                if (c < ncols) z[c] += v0;
+                if (c + 1 < ncols) z[c + 1] += v1;
+            }
+        });
+    }, smem);
 }
 
 // Γ[(ijk)][n'] = Σ_s Z_s[ij][k][n'] + Z_s[ik][j][n'] + Z_s[jk][i][n']   (splits in order)
@@ -662,8 +713,38 @@ static void prof_mark(mg_plan* P, int tag, cudaStream_t st) {
     ++P->prof_used;
 }
 
+// Side-stream operand kernels: (start, end) event pairs, summed into prof_ms[6].
+static void prof_side(mg_plan* P, cudaStream_t ss, bool start) {
+    if (!P->profile) return;
+    if (P->side_used == P->side_events.size()) {
+        cudaEvent_t e;
+        MG_CUDA(cudaEventCreate(&e));
+        P->side_events.push_back(e);
+    }
+    MG_CUDA(cudaEventRecord(P->side_events[P->side_used++], ss));
+    (void)start;
+}
+
+// Pipeline streams and dependency events, created once per plan on its device.
+static void plan_streams(mg_plan* P) {
+    if (P->ms) return;
+    int least = 0, greatest = 0;
+    MG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    MG_CUDA(cudaStreamCreateWithPriority(&P->ms, cudaStreamNonBlocking, greatest));
+    MG_CUDA(cudaStreamCreateWithPriority(&P->ss, cudaStreamNonBlocking, least));
+    for (cudaEvent_t* e : {&P->ev_start[0], &P->ev_start[1], &P->ev_end[0], &P->ev_end[1],
+                           &P->ev_panel[0], &P->ev_panel[1], &P->ev_s, &P->ev_x})
+        MG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
 static void prof_collect(mg_plan* P) {
     if (!P->profile) return;
+    for (size_t i = 0; i + 1 < P->side_used; i += 2) {
+        float ms = 0.f;
+        MG_CUDA(cudaEventElapsedTime(&ms, P->side_events[i], P->side_events[i + 1]));
+        P->prof_ms[6] += ms;
+    }
+    P->side_used = 0;
     for (size_t i = 0; i + 1 < P->prof_used; ++i) {
         float ms = 0.f;
         MG_CUDA(cudaEventElapsedTime(&ms, P->prof_events[i], P->prof_events[i + 1]));
@@ -754,8 +835,6 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     const int nb1 = P->nb1, nb3 = P->nb3;
     const int pp = p * p;
     const int ncols = p * nm;
-    const int64_t ldr = round_up(ncols, 2);
-    const int ldq = (int)round_up(P2, 2);
 
     MgPrepared& pre = P->prep;
     if (!pre.valid) prepare_batches(P, hrows, hzoff, st);
@@ -763,33 +842,35 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     const std::vector<int>& tile_first = pre.tile_first;
     const int max_tile_rows = pre.max_tile_rows;
     const int64_t maxzt = pre.maxzt, maxpanel = pre.maxpanel;
-    (void)tiles;
-    if (dt1) P->sc->ZT.ensure(maxzt);
-    P->sc->panel.ensure(maxpanel);
+    if (dt1) P->sc->ZT.ensure(2 * maxzt);
+    P->sc->panel.ensure(2 * maxpanel);
     const size_t hsize = (size_t)nb1 * pp * (NxP / X_BK) * X_LDK;
-    if (P->sc->H.n < hsize) {  // x pads of H are never written: zero them once
-        P->sc->H.ensure(hsize);
-        MG_CUDA(cudaMemsetAsync(P->sc->H.p, 0, P->sc->H.n * sizeof(double), st));
-    }
+    const bool zero_h = P->sc->H.n < hsize;  // x pads of H are never written: zero them once
+    if (zero_h) P->sc->H.ensure(hsize);
     P->sc->G.ensure((size_t)nb3 * pp * P2);
+    // pair contraction operands in tile-blocked layouts, kp rows per block (K padded to BK)
+    const int64_t kp = round_up(nb3, RUN_BK);
+    const int mt3 = ceil_div(P2, RUN_TM), nt3 = ceil_div(ncols, RUN_TN);
+    P->sc->R.ensure((size_t)nt3 * kp * RUN_LDB);
     P->sc->S.ensure((size_t)nb1 * P2 * (NxP / X_BK) * X_LDK);
-    P->sc->R.ensure((size_t)nb3 * ldr);
-    P->sc->Sq.ensure((size_t)nb3 * ldq);
-    // K-split of the pair contraction so that its grid fills the 148 SMs
-    const int tiles3 = ceil_div(ncols, Cfg128::BN) * ceil_div(P2, Cfg128::BM);
+    P->sc->Sq.ensure((size_t)mt3 * kp * RUN_LDA);
+    int num_sms = 148;
+    MG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, P->device));
+    // K-split of the pair contraction (Z copies, summed in order by k_final) so that its
+    // persistent items fill the SMs evenly
     int nsplit = 1;
     {
         double best = 0;
+        const int tiles3 = mt3 * nt3;
         for (int s = 1; s <= 8; ++s) {
-            int ctas = tiles3 * s;
-            double eff = (double)ctas / (ceil_div(ctas, 148) * 148.0);
-            if (s > 1 && nb3 / s < 4 * PAIR_BK) break;
+            const int items = tiles3 * s;
+            const double eff = (double)items / (ceil_div(items, num_sms) * (double)num_sms);
+            if (s > 1 && nb3 / s < 4 * RUN_BK) break;
             if (eff > best + 0.02) { best = eff; nsplit = s; }
         }
     }
     const int64_t zsplit = (int64_t)P2 * ncols;
     P->sc->Z.ensure((size_t)nsplit * zsplit);
-    MG_CUDA(cudaMemsetAsync(P->sc->Z.p, 0, (size_t)nsplit * zsplit * sizeof(double), st));
     P->gamma.ensure((size_t)nm * nm);
 
     static bool attr_done_dev[64] = {false};  // function attributes are per device context
@@ -799,7 +880,6 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     const size_t smem_x = xt == XTile::T120   ? XPipeP<CfgX120>::smem_bytes
                           : xt == XTile::T160 ? XPipeP<CfgX160>::smem_bytes
                                               : XPipeP<CfgX128>::smem_bytes;
-    const size_t smem_pair = PairPipe::smem_bytes;
     if (!attr_done) {
         MG_CUDA(cudaFuncSetAttribute(k_run_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_run));
@@ -813,99 +893,177 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)XPipeP<CfgX128>::smem_bytes));
         MG_CUDA(cudaFuncSetAttribute(k_pair_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_pair));
+                                     (int)smem_run));
         attr_done = true;
     }
-    DBuf<int> l0d;
-    l0d.upload(P->l0, 2, st);
-    int num_sms = 148;
-    MG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, P->device));
+
+    // Streams: the contractions run on the plan's high-priority stream `ms`; the operand
+    // kernels (A panels of the run contraction, pair products of the x contraction) run on
+    // the low-priority side stream `ss`, one batch ahead, in the registers/threads the
+    // persistent contraction CTA leaves free on each SM.  Panels (and explicit-triple weights)
+    // are double-buffered; S is single-buffered (pair products of batch i start once the x
+    // contraction of batch i-1 has consumed S, i.e. while the run contraction of batch i runs).
+    plan_streams(P);
+    cudaStream_t ms = P->ms, ss = P->ss;
+    MG_CUDA(cudaEventRecord(P->ev_start[0], st));
+    MG_CUDA(cudaEventRecord(P->ev_start[1], 0));  // scratch allocations are ordered on stream 0
+    for (cudaStream_t x : {ms, ss})
+        for (int k = 0; k < 2; ++k) MG_CUDA(cudaStreamWaitEvent(x, P->ev_start[k], 0));
+    if (zero_h) MG_CUDA(cudaMemsetAsync(P->sc->H.p, 0, P->sc->H.n * sizeof(double), ms));
+    MG_CUDA(cudaMemsetAsync(P->sc->Z.p, 0, (size_t)nsplit * zsplit * sizeof(double), ms));
+    P->l0d.upload(P->l0, 2, ms);
+    MG_CUDA(cudaStreamSynchronize(ms));  // l0 comes from pageable host memory
+    prof_mark(P, 0, ms);
+
+    struct Batch { int64_t b1, e1, b3, e3; int bidx; };
+    std::vector<Batch> batches;
+    {
+        int bidx = 0;
+        for (int64_t b3 = 0; b3 < nrows; b3 += nb3) {
+            const int64_t e3 = std::min<int64_t>(b3 + nb3, nrows);
+            for (int64_t b1 = b3; b1 < e3; b1 += nb1, ++bidx)
+                batches.push_back({b1, std::min<int64_t>(b1 + nb1, e3), b3, e3, bidx});
+        }
+    }
+    double* panel_buf[2] = {P->sc->panel.p, P->sc->panel.p + maxpanel};
+    double* zt_buf[2] = {dt1 ? P->sc->ZT.p : nullptr, dt1 ? P->sc->ZT.p + maxzt : nullptr};
+    // operands of batch k: explicit-triple weights + A panels (buffer k % 2), on stream `os`
+    auto issue_panels = [&](int k, cudaStream_t os) {
+        const Batch& B = batches[k];
+        const int64_t zbase = hzoff[B.b1];
+        const double* zt = nullptr;
+        if (dt1) {
+            double* ztb = zt_buf[k & 1];
+            const int64_t t0 = (*tri_of_row)[B.b1], t1 = (*tri_of_row)[B.e1];
+            MG_CUDA(cudaMemsetAsync(ztb, 0, (hzoff[B.e1] - zbase) * sizeof(double), os));
+            if (t1 > t0)
+                k_scatter_weights<<<std::min<int64_t>((t1 - t0 + 255) / 256, 4096), 256, 0, os>>>(
+                    dt1 + t0, dt2 + t0, dt3 + t0, dpos + t0, ddup + t0, t1 - t0, zbase, P->l_min,
+                    P->C.p, P->v.p, P->lf.p, P->h2_mode, ztb);
+            MG_LAUNCHED();
+            zt = ztb;
+        }
+        const int tf = tile_first[B.bidx], tl = tile_first[B.bidx + 1];
+        int nch = 1;
+        for (int t = tf; t < tl; ++t)
+            nch = std::max(nch, ceil_div(round_up(tiles[t].jhi - tiles[t].jlo + 1, RUN_BK), PANEL_JC));
+        k_run_panels<<<dim3(tl - tf, nch), PANEL_THREADS, max_tile_rows * PANEL_JC * sizeof(double),
+                       os>>>(
+            P->prep.tiles_d.p + tf, P->prep.rows.p, P->prep.poff.p + tf, P->prep.zoff.p, zbase,
+            zt, P->l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p, P->fl.p,
+            P->h2_mode, panel_buf[k & 1]);
+        MG_LAUNCHED();
+    };
+
+    auto issue_pairs = [&](int k, cudaStream_t os) {
+        const Batch& B = batches[k];
+        dim3 gs(ceil_div(P2, PP_CHUNK), (int)(B.e1 - B.b1));
+        k_pair_products<<<gs, 256, 0, os>>>(P->prep.rows.p, (int)B.b1, P->QT.p, p, P2, NxP,
+                                             P->l_min, P->sc->S.p);
+        MG_LAUNCHED();
+    };
 
     double f_run = 0, f_x = 0, f_pair = 0;
     int64_t launches = 0;
-    int bidx = 0;
-    for (int64_t b3 = 0; b3 < nrows; b3 += nb3) {
-        int64_t e3 = std::min<int64_t>(b3 + nb3, nrows);
-        for (int64_t b1 = b3; b1 < e3; b1 += nb1, ++bidx) {
-            int64_t e1 = std::min<int64_t>(b1 + nb1, e3);
-            int nb = (int)(e1 - b1);
-            const int64_t zbase = hzoff[b1];
-            const double* zt = nullptr;
-            if (dt1) {
-                int64_t t0 = (*tri_of_row)[b1], t1 = (*tri_of_row)[e1];
-                MG_CUDA(cudaMemsetAsync(P->sc->ZT.p, 0, (hzoff[e1] - zbase) * sizeof(double), st));
-                if (t1 > t0)
-                    k_scatter_weights<<<std::min<int64_t>((t1 - t0 + 255) / 256, 4096), 256, 0,
-                                        st>>>(dt1 + t0, dt2 + t0, dt3 + t0, dpos + t0, ddup + t0,
-                                              t1 - t0, zbase, P->l_min, P->C.p, P->v.p,
-                                              P->lf.p, P->h2_mode, P->sc->ZT.p);
-                MG_LAUNCHED();
-                zt = P->sc->ZT.p;
-            }
-            int tf = tile_first[bidx], tl = tile_first[bidx + 1];
-            prof_mark(P, 0, st);
-            k_run_panels<<<tl - tf, PANEL_THREADS, max_tile_rows * PANEL_JC * sizeof(double),
-                           st>>>(P->prep.tiles_d.p + tf, P->prep.rows.p, P->prep.poff.p + tf, P->prep.zoff.p, zbase, zt,
-                                 l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p,
-                                 P->fl.p, P->h2_mode, P->sc->panel.p);
-            MG_LAUNCHED();
-            {
-                dim3 gs(ceil_div(P2, PP_CHUNK), nb);
-                k_pair_products<<<gs, 256, 0, st>>>(P->prep.rows.p, (int)b1, P->QT.p, p, P2, NxP,
-                                                    P->l_min, P->sc->S.p);
-                MG_LAUNCHED();
-            }
-            prof_mark(P, 1, st);
-            k_run_contract<<<num_sms, RunPipeP::THREADS, smem_run, st>>>(
-                P->prep.tiles_d.p + tf, tl - tf, P->prep.poff.p + tf, P->sc->panel.p, (int)b1, P->prep.rows.p,
-                P->WQT.p, p, P->Nx, P->Nxw, NxP, make_longlong2(P->wbase[0], P->wbase[1]),
-                make_int2(P->wrows[0], P->wrows[1]), P->sc->H.p);
-            MG_LAUNCHED();
-            prof_mark(P, 2, st);
-            if (xt == XTile::T120) {
-                k_x_contract_p<CfgX120><<<num_sms, XPipeP<CfgX120>::THREADS, smem_x, st>>>(
-                    P->sc->S.p, P->sc->H.p, nb, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
-            } else if (xt == XTile::T160) {
-                k_x_contract_p<CfgX160><<<num_sms, XPipeP<CfgX160>::THREADS, smem_x, st>>>(
-                    P->sc->S.p, P->sc->H.p, nb, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
-            } else {
-                k_x_contract_p<CfgX128><<<num_sms, XPipeP<CfgX128>::THREADS, smem_x, st>>>(
-                    P->sc->S.p, P->sc->H.p, nb, (int)b1, (int)b3, p, P2, P->Nx, NxP, P->sc->G.p);
-            }
-            MG_LAUNCHED();
-            launches += 4 + (dt1 ? 1 : 0);
-            for (int64_t r = b1; r < e1; ++r) {
-                double m = (double)(hrows[r].jhi - hrows[r].jlo + 1);
-                f_run += 2.0 * p * p * P->Nx * m;
-            }
-            f_x += 2.0 * P2 * pp * P->Nx * (double)nb;
+    const int nbat = (int)batches.size();
+    for (int k = 0; k < nbat; ++k) {
+        const Batch& B = batches[k];
+        const int nb = (int)(B.e1 - B.b1);
+        const int tf = tile_first[B.bidx], tl = tile_first[B.bidx + 1];
+#if MG_SIDE
+        // side stream, once x(k-1) has consumed S: pair products of batch k (and, MG_SIDE 2,
+        // the panels of batch k), beside the run contraction of batch k
+        if (k > 0) MG_CUDA(cudaStreamWaitEvent(ss, P->ev_x, 0));
+        prof_side(P, ss, true);
+        issue_pairs(k, ss);
+        prof_side(P, ss, false);
+        MG_CUDA(cudaEventRecord(P->ev_s, ss));
+#if MG_SIDE == 2
+        if (k == 0) {
+            issue_panels(0, ss);
+            MG_CUDA(cudaEventRecord(P->ev_panel[0], ss));
         }
-        const int n3 = (int)(e3 - b3);
-        prof_mark(P, 3, st);
-        dim3 gg(std::min(ceil_div(ncols, 256), 64), n3);
-        k_gather<<<gg, 256, 0, st>>>(P->prep.rows.p + b3, P->sc->G.p, P->modes.p, P->q.p, P->L, P->l_min,
-                                     p, P2, nm, ldr, ldq, P->sc->R.p, P->sc->Sq.p);
+        if (k + 1 < nbat) {  // into the buffer run(k-1) read (run(k-1) precedes x(k-1))
+            prof_side(P, ss, true);
+            issue_panels(k + 1, ss);
+            prof_side(P, ss, false);
+            MG_CUDA(cudaEventRecord(P->ev_panel[(k + 1) & 1], ss));
+        }
+        prof_mark(P, 0, ms);
+        MG_CUDA(cudaStreamWaitEvent(ms, P->ev_panel[k & 1], 0));
+#else
+        prof_mark(P, 0, ms);
+        issue_panels(k, ms);
+#endif
+#else
+        prof_mark(P, 0, ms);
+        issue_pairs(k, ms);
+        issue_panels(k, ms);
+#endif
+        prof_mark(P, 1, ms);
+        k_run_contract<<<num_sms, RunPipeP::THREADS, smem_run, ms>>>(
+            P->prep.tiles_d.p + tf, tl - tf, P->prep.poff.p + tf, panel_buf[k & 1], (int)B.b1,
+            P->prep.rows.p, P->WQT.p, p, P->Nx, P->Nxw, NxP,
+            make_longlong2(P->wbase[0], P->wbase[1]), make_int2(P->wrows[0], P->wrows[1]),
+            P->sc->H.p);
         MG_LAUNCHED();
-        const int per = (int)round_up(ceil_div(n3, nsplit), PAIR_BK);
-        dim3 g3(ceil_div(ncols, Cfg128::BN), ceil_div(P2, Cfg128::BM), ceil_div(n3, per));
-        prof_mark(P, 4, st);
-        k_pair_contract<<<g3, 256, smem_pair, st>>>(P->sc->Sq.p, ldq, P->sc->R.p, ldr, n3, per,
-                                                           P2, ncols, zsplit, P->sc->Z.p);
+#if MG_SIDE
+        prof_mark(P, 0, ms);
+        MG_CUDA(cudaStreamWaitEvent(ms, P->ev_s, 0));
+#endif
+        prof_mark(P, 2, ms);
+        if (xt == XTile::T120) {
+            k_x_contract_p<CfgX120><<<num_sms, XPipeP<CfgX120>::THREADS, smem_x, ms>>>(
+                P->sc->S.p, P->sc->H.p, nb, (int)B.b1, (int)B.b3, p, P2, P->Nx, NxP, P->sc->G.p);
+        } else if (xt == XTile::T160) {
+            k_x_contract_p<CfgX160><<<num_sms, XPipeP<CfgX160>::THREADS, smem_x, ms>>>(
+                P->sc->S.p, P->sc->H.p, nb, (int)B.b1, (int)B.b3, p, P2, P->Nx, NxP, P->sc->G.p);
+        } else {
+            k_x_contract_p<CfgX128><<<num_sms, XPipeP<CfgX128>::THREADS, smem_x, ms>>>(
+                P->sc->S.p, P->sc->H.p, nb, (int)B.b1, (int)B.b3, p, P2, P->Nx, NxP, P->sc->G.p);
+        }
+        MG_LAUNCHED();
+        MG_CUDA(cudaEventRecord(P->ev_x, ms));
+        launches += 4 + (dt1 ? 1 : 0);
+        for (int64_t r = B.b1; r < B.e1; ++r) {
+            double m = (double)(hrows[r].jhi - hrows[r].jlo + 1);
+            f_run += 2.0 * p * p * P->Nx * m;
+        }
+        f_x += 2.0 * P2 * pp * P->Nx * (double)nb;
+        if (B.e1 != B.e3) continue;
+        // end of a pair-contraction group: gather + pair contraction over its rows
+        const int n3 = (int)(B.e3 - B.b3);
+        prof_mark(P, 3, ms);
+        dim3 gg(std::min(ceil_div(ncols, 256), 64), (int)round_up(n3, RUN_BK));
+        k_gather<<<gg, 256, 0, ms>>>(P->prep.rows.p + B.b3, P->sc->G.p, P->modes.p, P->q.p, P->L,
+                                     P->l_min, p, P2, nm, n3, kp, P->sc->R.p, P->sc->Sq.p);
+        MG_LAUNCHED();
+        const int per = (int)round_up(ceil_div(n3, nsplit), RUN_BK);
+        prof_mark(P, 4, ms);
+        k_pair_contract<<<num_sms, RunPipeP::THREADS, smem_run, ms>>>(
+            P->sc->Sq.p, P->sc->R.p, kp, n3, per, ceil_div(n3, per), P2, ncols, zsplit,
+            P->sc->Z.p);
         MG_LAUNCHED();
         launches += 2;
         f_pair += 2.0 * P2 * ncols * (double)n3;
     }
-    prof_mark(P, 5, st);
-    k_final<<<std::min<int64_t>(((int64_t)nm * nm + 255) / 256, 4096), 256, 0, st>>>(
+    prof_mark(P, 5, ms);
+    k_final<<<std::min<int64_t>(((int64_t)nm * nm + 255) / 256, 4096), 256, 0, ms>>>(
         P->sc->Z.p, nsplit, zsplit, P->modes.p, p, nm, P->gamma.p);
     MG_LAUNCHED();
-    prof_mark(P, -1, st);
+    prof_mark(P, -1, ms);
     launches += 1;
     P->flops_run = f_run;
     P->flops_x = f_x;
     P->flops_pair = f_pair;
     P->launches = launches;
-    MG_CUDA(cudaStreamSynchronize(st));  // keeps l0d alive until the stream drains
+    // the caller's stream (and stream 0, which frees/reallocates scratch) resume after both
+    MG_CUDA(cudaEventRecord(P->ev_end[0], ms));
+    MG_CUDA(cudaEventRecord(P->ev_end[1], ss));
+    for (cudaStream_t x : {st, (cudaStream_t)0})
+        for (int k = 0; k < 2; ++k) MG_CUDA(cudaStreamWaitEvent(x, P->ev_end[k], 0));
+    MG_CUDA(cudaStreamSynchronize(ms));
+    MG_CUDA(cudaStreamSynchronize(ss));
     prof_collect(P);
 }
 

@@ -20,7 +20,7 @@ struct MgTile {
     int row0, c0, nslots, nrows, jlo, jhi, pad0, pad1;
 };
 
-constexpr int MG_NPROF = 6;
+constexpr int MG_NPROF = 7;
 
 // Batch scratch, pooled per device so that one-shot calls (the drop-in API) do not pay for
 // allocating and zeroing gigabytes every time.  Buffers only grow; they are zeroed when
@@ -67,14 +67,28 @@ struct mg_plan {
     // stats of the last execute
     double flops_run = 0, flops_x = 0, flops_pair = 0;
     int64_t launches = 0;
-    // optional kernel timing: ms per family {panels, run, x, gather, pair, final}
+    // optional kernel timing: ms per family {exposed operand wait, run, x, gather, pair,
+    // final, side-stream operand kernels (overlapped)}
     bool profile = false;
-    double prof_ms[MG_NPROF] = {0, 0, 0, 0, 0, 0};
+    double prof_ms[MG_NPROF] = {0, 0, 0, 0, 0, 0, 0};
     std::vector<cudaEvent_t> prof_events;
     std::vector<int> prof_tags;
     size_t prof_used = 0;
+    std::vector<cudaEvent_t> side_events;  // (start, end) pairs on the side stream
+    size_t side_used = 0;
+    // streams/events of the batch pipeline (created on first execute, on the plan's device)
+    cudaStream_t ms = nullptr, ss = nullptr;
+    cudaEvent_t ev_start[2] = {}, ev_end[2] = {}, ev_panel[2] = {};
+    cudaEvent_t ev_s = nullptr, ev_x = nullptr;
+    mg::DBuf<int> l0d;
     ~mg_plan() {
         for (auto e : prof_events) cudaEventDestroy(e);
+        for (auto e : side_events) cudaEventDestroy(e);
+        for (cudaEvent_t e : {ev_start[0], ev_start[1], ev_end[0], ev_end[1], ev_panel[0],
+                              ev_panel[1], ev_s, ev_x})
+            if (e) cudaEventDestroy(e);
+        if (ms) cudaStreamDestroy(ms);
+        if (ss) cudaStreamDestroy(ss);
     }
     // host copies (for the direct/nonsep paths)
     std::vector<double> hC, hv;

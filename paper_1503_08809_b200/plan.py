@@ -76,9 +76,10 @@ class GammaPlan:
         nat.check(nat.lib().mg_plan_set_profile(self._h, int(bool(on))))
 
     def kernel_ms(self) -> dict:
-        ms = np.zeros(6)
+        ms = np.zeros(7)
         nat.check(nat.lib().mg_plan_kernel_ms(self._h, nat.ptr(ms)))
-        return dict(zip(("operands", "run", "x", "gather", "pair", "final"), ms.tolist()))
+        return dict(zip(("operands", "run", "x", "gather", "pair", "final", "operands_side"),
+                        ms.tolist()))
 
     def close(self):
         if self._h:

@@ -57,6 +57,65 @@ __global__ void dmma16816_k(double* out, int iters){
   if(r==12345.678) out[0]=r;
 }
 
+
+// Mixed: every warp interleaves 8 DMMA (acc8) with R x 8 independent DFMA chains, to see
+// whether the DMMA and DFMA paths share one FP64 datapath (time = sum) or not (time = max).
+template<int R>
+__global__ void mixed_k(double* out, int iters, double s){
+  double c[8][2];
+  #pragma unroll
+  for(int i=0;i<8;i++){c[i][0]=0;c[i][1]=0;}
+  double f[8];
+  #pragma unroll
+  for(int i=0;i<8;i++) f[i]=threadIdx.x*1e-3+i;
+  double a=1.0+threadIdx.x*1e-6, b=1.0-threadIdx.x*1e-6, m=1.0000001;
+  for(int it=0; it<iters; ++it){
+    #pragma unroll
+    for(int i=0;i<8;i++){
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c[i][0]),"+d"(c[i][1]) : "d"(a),"d"(b));
+      #pragma unroll
+      for(int r=0;r<R;r++) f[(i+r)&7]=fma(f[(i+r)&7],m,s);
+    }
+  }
+  double r=0;
+  #pragma unroll
+  for(int i=0;i<8;i++) r+=c[i][0]+c[i][1]+f[i];
+  if(r==12345.678) out[0]=r;
+}
+// Split: even warps DMMA only, odd warps DFMA only (same per-warp flop count).
+__global__ void split_k(double* out, int iters, double s){
+  if(((threadIdx.x>>5)&1)==0){
+    double c[8][2];
+    #pragma unroll
+    for(int i=0;i<8;i++){c[i][0]=0;c[i][1]=0;}
+    double a=1.0+threadIdx.x*1e-6, b=1.0-threadIdx.x*1e-6;
+    for(int it=0; it<iters; ++it){
+      #pragma unroll
+      for(int i=0;i<8;i++)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+          : "+d"(c[i][0]),"+d"(c[i][1]) : "d"(a),"d"(b));
+    }
+    double r=0;
+    #pragma unroll
+    for(int i=0;i<8;i++) r+=c[i][0]+c[i][1];
+    if(r==12345.678) out[0]=r;
+  } else {
+    double f[8];
+    #pragma unroll
+    for(int i=0;i<8;i++) f[i]=threadIdx.x*1e-3+i;
+    double m=1.0000001;
+    for(int it=0; it<iters*8; ++it){
+      #pragma unroll
+      for(int i=0;i<8;i++) f[i]=fma(f[i],m,s);
+    }
+    double r=0;
+    #pragma unroll
+    for(int i=0;i<8;i++) r+=f[i];
+    if(r==12345.678) out[0]=r;
+  }
+}
+
 int main(){
   int dev=0; cudaDeviceProp p; CK(cudaGetDeviceProperties(&p,dev));
   int clk=0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
@@ -86,6 +145,14 @@ int main(){
     char nm[96]; snprintf(nm,96,"DMMA 16x8x16 acc4 tpb%d bps%d",tpb,bps);
     int blocks=sms*bps;
     run(nm, [&]{dmma16816_k<4><<<blocks,tpb>>>(out,it/4);}, 2.0*2048*4*(it/4)*(double)blocks*(tpb/32));
+  }
+  {
+    int blocks=sms*2, tpb=256;
+    // per warp per iter: 8 DMMA = 4096 flop; R*8 DFMA*32 lanes*2 = 512 R flop
+    run("MIXED dmma8 + dfma x8 (R=8)", [&]{mixed_k<8><<<blocks,tpb>>>(out,it,1e-9);}, (4096.0+512*8)*it*(double)blocks*(tpb/32));
+    run("MIXED dmma8 + dfma x4 (R=4)", [&]{mixed_k<4><<<blocks,tpb>>>(out,it,1e-9);}, (4096.0+512*4)*it*(double)blocks*(tpb/32));
+    run("MIXED dmma8 + dfma x2 (R=2)", [&]{mixed_k<2><<<blocks,tpb>>>(out,it,1e-9);}, (4096.0+512*2)*it*(double)blocks*(tpb/32));
+    run("SPLIT warps dmma | dfma", [&]{split_k<<<blocks,tpb>>>(out,it,1e-9);}, (4096.0*4+ 8.0*8*2*32*4)*it*(double)blocks);
   }
   for(int acc : {1,2,4}){
     char nm[96]; snprintf(nm,96,"DMMA 8x8x4 acc%d tpb256 bps2 (latency)",acc);
