@@ -130,9 +130,10 @@ int mg_plan_stats(mg_plan* plan, double* flops_rowcontract, double* flops_xcontr
                   double* flops_pairs, int64_t* launches);
 /* Per-kernel-family timing with CUDA events on the launching stream (bench roofline):
  * after mg_plan_set_profile(plan, 1), every execute accumulates milliseconds into
- * ms[7] = {exposed wait of the contractions for their operands, run contraction,
+ * ms[8] = {exposed wait of the contractions for their operands, run contraction,
  *          x contraction, R gather, pair contraction, final,
- *          operand kernels (A panels, pair products) on the side stream, overlapped}. */
+ *          operand kernels (A panels, pair products) on the side stream, overlapped,
+ *          non-separable kernels (mg_plan_nonsep)}. */
 int mg_plan_set_profile(mg_plan* plan, int on);
 int mg_plan_kernel_ms(mg_plan* plan, double* ms);
 void mg_plan_destroy(mg_plan* plan);
@@ -174,6 +175,15 @@ int mg_gamma_nonsep(const double* q, const double* qt, const double* C, const do
                     int l_max, int h2_mode, const double* alpha, const int32_t* l1,
                     const int32_t* l2, const int32_t* l3, const double* W, int64_t count,
                     int device, double* b);
+/* Resident form of the same path (tables of an mg_plan, sparse domain uploaded once):
+ * mg_plan_set_sparse_domain validates and uploads (l1,l2,l3,W)[count]; mg_plan_nonsep
+ * evaluates b for one alpha [n] (host) on `stream` into b_dev (device, optional) and/or
+ * b_host (host, optional; synchronises).  With profiling on, kernel time accumulates in
+ * mg_plan_kernel_ms()[7]. */
+int mg_plan_set_sparse_domain(mg_plan* plan, const int32_t* l1, const int32_t* l2,
+                              const int32_t* l3, const double* W, int64_t count);
+int mg_plan_nonsep(mg_plan* plan, const double* alpha, double* b_dev, double* b_host,
+                   void* stream);
 
 /* ---------------------------------------------------------------------------------------
  * μ-quadrature ("separable", Modal2D) engine: replaces build_ptable / gamma2d_matrix

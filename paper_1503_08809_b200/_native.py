@@ -47,6 +47,8 @@ _SIGS = {
     "mg_plan_set_profile": (_i, [_vp, _i]),
     "mg_plan_kernel_ms": (_i, [_vp, _vp]),
     "mg_plan_destroy": (None, [_vp]),
+    "mg_plan_set_sparse_domain": (_i, [_vp, _vp, _vp, _vp, _vp, _i64]),
+    "mg_plan_nonsep": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "mg_build_qtilde": (_i, [_vp, _vp, _i, _vp, _i, _vp, _vp, _i, _i, _i, _d, _d, _d, _i, _vp,
                              _vp, _vp]),
     "mg_build_qtilde_dev": (_i, [_vp, _vp, _i, _vp, _i, _vp, _vp, _i, _i, _i, _d, _d, _d, _i,
@@ -74,7 +76,10 @@ def lib():
                 f"{LIB_PATH} is missing: build it with `python -m paper_1503_08809_b200.build` "
                 "(there is no CPU fallback)")
         handle = ctypes.CDLL(LIB_PATH)
+        variant = "MG_LIB_PATH" in os.environ   # tuning variants may predate newer symbols
         for name, (res, args) in _SIGS.items():
+            if variant and not hasattr(handle, name):
+                continue
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

@@ -219,6 +219,28 @@ int mg_plan_kernel_ms(mg_plan* P, double* ms) {
     });
 }
 
+int mg_plan_set_sparse_domain(mg_plan* P, const int32_t* l1, const int32_t* l2,
+                              const int32_t* l3, const double* W, int64_t count) {
+    return guarded([&] {
+        MG_REQUIRE(P, "null plan");
+        MG_REQUIRE(count >= 0, "count must be >= 0");
+        MG_REQUIRE(count == 0 || (l1 && l2 && l3 && W), "null triple arrays");
+        DeviceGuard g(P->device);
+        nonsep_set_domain(P, l1, l2, l3, W, count);
+    });
+}
+
+int mg_plan_nonsep(mg_plan* P, const double* alpha, double* b_dev, double* b_host,
+                   void* stream) {
+    return guarded([&] {
+        MG_REQUIRE(P && alpha, "null argument");
+        for (int i = 0; i < P->nm; ++i)
+            MG_REQUIRE(std::isfinite(alpha[i]), "alpha contains non-finite values");
+        DeviceGuard g(P->device);
+        nonsep_execute(P, alpha, b_dev, b_host, (cudaStream_t)stream);
+    });
+}
+
 void mg_plan_destroy(mg_plan* P) {
     if (!P) return;
     int prev = -1;

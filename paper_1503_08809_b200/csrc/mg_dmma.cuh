@@ -407,13 +407,21 @@ struct PipeTMAPersistent {
                 b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g4);
         };
         int g = 0;
+        // item metadata (k-tile count, valid k of the last tile) is read one item ahead, so
+        // its global-load latency hides under the current item's DMMAs
+        int kts_n = first < nitems ? prod.ktiles(first) : 0;
+        int kvl_n = first < nitems ? prod.kvalid_last(first) : 0;
         for (int it = first; it < nitems; it += stride) {
 #pragma unroll
             for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < FN; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
-            const int kts = prod.ktiles(it);
-            const int kvl = prod.kvalid_last(it);
+            const int kts = kts_n;
+            const int kvl = kvl_n;
+            if (it + stride < nitems) {
+                kts_n = prod.ktiles(it + stride);
+                kvl_n = prod.kvalid_last(it + stride);
+            }
             {
                 const int s = g % STAGES;
                 mbar_wait(full + s, (g / STAGES) & 1);

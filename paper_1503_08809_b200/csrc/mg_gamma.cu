@@ -97,6 +97,9 @@ __global__ void k_scatter_weights(const int32_t* __restrict__ t1, const int32_t*
 #ifndef MG_SIDE  // operand kernels on the side stream: 0 none, 1 pair products, 2 + panels
 #define MG_SIDE 1
 #endif
+#ifndef MG_NO_EPI
+#define MG_NO_EPI 0  // diagnostics only: 1 skips the run/x contraction output stores
+#endif
 #ifndef MG_RUN_BK
 #define MG_RUN_BK 32
 #define MG_RUN_ST 3
@@ -236,7 +239,7 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
         const int ti = it / items.NB, nb = it - ti * items.NB;
         const MgTile tl = tiles[ti];
         const int n0 = nb * RUN_TN;
-        const int64_t hbase = (int64_t)(tl.row0 - row_base) * p + tl.c0;  // H row of slot 0
+        const int hbase = (tl.row0 - row_base) * p + tl.c0;  // H row of slot 0
         // Per-thread offsets, computed once per item (no divisions in the store loop):
         // slot (rr, c) -> (rr*XB*pp + c*p)*X_LDK ; column gn = c'*Nxw + x ->
         // ((x/32)*pp + c')*X_LDK + x%32   (Nxw even: columns gn, gn+1 share c' and x-block)
@@ -248,9 +251,9 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
 #pragma unroll
         for (int fm = 0; fm < CfgRun::FM; ++fm) {
             const int m = wm + fm * 8;
-            const int64_t slot = hbase + m, rr = slot / p;
+            const int slot = (int)hbase + m, rr = slot / p;  // < nb1 * p: 32-bit division
             rok[fm] = m < tl.nslots;
-            roff[fm] = (rr * XB * pp + (slot - rr * p) * p) * X_LDK;
+            roff[fm] = ((int64_t)rr * XB * pp + (int64_t)(slot - rr * p) * p) * X_LDK;
         }
 #pragma unroll
         for (int fn = 0; fn < CfgRun::FN; ++fn) {
@@ -260,7 +263,7 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
             const int64_t coff = ((int64_t)(x / X_BK) * pp + cp) * X_LDK + (x & (X_BK - 1));
 #pragma unroll
             for (int fm = 0; fm < CfgRun::FM; ++fm) {
-                if (!rok[fm]) continue;
+                if (!rok[fm] || MG_NO_EPI) continue;
                 double* h = H + roff[fm] + coff;
                 if (both) {
                     *reinterpret_cast<double2*>(h) =
@@ -287,7 +290,7 @@ __device__ __forceinline__ void pair_of(int pr, int& a, int& b) {
     b = bb;
     a = pr - bb * (bb + 1) / 2;
 }
-__device__ __forceinline__ int pair_idx(int a, int b) {  // a <= b
+__host__ __device__ __forceinline__ int pair_idx(int a, int b) {  // a <= b
     return b * (b + 1) / 2 + a;
 }
 
@@ -397,7 +400,7 @@ k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int n
         double* Gr = G + (int64_t)(row_b1 + r - row_b3) * pp * P2;
         acc_foreach_pair<Cfg>(acc, [&](int m, int n, double v0, double v1) {
             const int prr = m0 + m, cc = n0 + n;
-            if (prr < P2) {
+            if (prr < P2 && !MG_NO_EPI) {
                 if (cc < pp) Gr[(int64_t)cc * P2 + prr] = v0;
                 if (cc + 1 < pp) Gr[(int64_t)(cc + 1) * P2 + prr] = v1;
             }
@@ -612,6 +615,7 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
     P->v.upload(v, L);
     P->wr2.upload(wr2, Nx);
     P->modes.upload(md.data(), md.size());
+    P->hmodes = md;
     std::vector<double> lf = log_factorials(3 * l_max + 2);
     P->lf.upload(lf.data(), lf.size());
 
@@ -1242,7 +1246,8 @@ void weights(int l_min, int l_max, const double* C, const double* v, int h2_mode
 }
 
 // ------------------------------------------------------------------------------------------
-// Non-separable pointwise path (config 3)
+// Non-separable pointwise path (config 3).  k_nonsep is the generic (any p, slow) kernel
+// used for p > 16; k_nonsep_warp below is the compile-time-P kernel.
 //   B(t,x) = Σ_n' α_n' Σ_6perms q̃q̃q̃  evaluated per (triple, x) — no factoring through Γ
 //   b[m]  += W_t zm_t P[m,t] Σ_x wr2_x B(t,x)
 // One CTA walks a strided subset of triples; per-CTA partial b's are summed in CTA order.
@@ -1250,8 +1255,7 @@ void weights(int l_min, int l_max, const double* C, const double* v, int h2_mode
 constexpr int NS_THREADS = 256;
 
 __global__ void __launch_bounds__(NS_THREADS)
-k_nonsep(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
-         const int32_t* __restrict__ t3, const double* __restrict__ W, int64_t count,
+k_nonsep(const int4* __restrict__ trip, const double* __restrict__ W, int64_t count,
          const double* __restrict__ QT, const double* __restrict__ wr2,
          const double* __restrict__ q, const double* __restrict__ C, const double* __restrict__ v,
          const double* __restrict__ lf, int mode, const double* __restrict__ alpha,
@@ -1272,7 +1276,8 @@ k_nonsep(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t t = blockIdx.x; t < count; t += gridDim.x) {
-        const int a1 = t1[t], a2 = t2[t], a3 = t3[t];
+        const int4 tr = trip[t];
+        const int a1 = tr.x, a2 = tr.y, a3 = tr.z;
         const double* g1 = QT + (int64_t)(a1 - l_min) * p * NxP;
         const double* g2 = QT + (int64_t)(a2 - l_min) * p * NxP;
         const double* g3 = QT + (int64_t)(a3 - l_min) * p * NxP;
@@ -1311,176 +1316,121 @@ k_nonsep(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
     for (int i = threadIdx.x; i < nm; i += blockDim.x) partial[(int64_t)blockIdx.x * nm + i] = b_acc[i];
 }
 
-// Faster pointwise kernel (p <= 16): per (triple, x) each thread stages q̃ at l1, l2, l3 and
-// the pair sums S_ab(x) = q̃_a(x,l2)q̃_b(x,l3) + q̃_b(x,l2)q̃_a(x,l3) in its own shared-memory
-// column, then sums the modes pointwise: B(t,x) = Σ_n' α_n' [q̃_k'(l1) S_i'j' + q̃_j'(l1) S_i'k'
-// + q̃_i'(l1) S_j'k'] (the 6-permutation product, no factoring through Γ).
-constexpr int NS2_THREADS = 128;
-
-__global__ void __launch_bounds__(NS2_THREADS)
-k_nonsep2(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
-          const int32_t* __restrict__ t3, const double* __restrict__ W, int64_t count,
-          const double* __restrict__ QT, const double* __restrict__ wr2,
-          const double* __restrict__ q, const double* __restrict__ C, const double* __restrict__ v,
-          const double* __restrict__ lf, int mode, const double* __restrict__ alpha,
-          const int* __restrict__ modes, int p, int nm, int Nx, int NxP, int L, int l_min,
-          double* __restrict__ partial) {
-    extern __shared__ double sh[];
-    const int P2 = p * (p + 1) / 2;
-    double* col = sh;                                   // [(3p + P2)][NS2_THREADS]
-    double* b_acc = col + (3 * p + P2) * NS2_THREADS;   // [nm]
-    double* al = b_acc + nm;                            // [nm]
-    double* red = al + nm;                              // [NS2_THREADS/32]
-    int* md = reinterpret_cast<int*>(red + NS2_THREADS / 32);  // [nm][6]: i j k, ij ik jk
-    for (int i = threadIdx.x; i < nm; i += blockDim.x) {
-        b_acc[i] = 0.0;
-        al[i] = alpha[i];
-        const int a = modes[3 * i], b = modes[3 * i + 1], c = modes[3 * i + 2];
-        md[6 * i] = a; md[6 * i + 1] = b; md[6 * i + 2] = c;
-        md[6 * i + 3] = pair_idx(a, b); md[6 * i + 4] = pair_idx(a, c); md[6 * i + 5] = pair_idx(b, c);
-    }
-    __syncthreads();
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double* q1 = col;                       // q̃(l1)[c]  at q1[c*T + tid]
-    double* q2 = col + p * NS2_THREADS;
-    double* q3 = col + 2 * p * NS2_THREADS;
-    double* S = col + 3 * p * NS2_THREADS;  // S[pair*T + tid]
-    for (int64_t t = blockIdx.x; t < count; t += gridDim.x) {
-        const int a1 = t1[t], a2 = t2[t], a3 = t3[t];
-        const double* g1 = QT + (int64_t)(a1 - l_min) * p * NxP;
-        const double* g2 = QT + (int64_t)(a2 - l_min) * p * NxP;
-        const double* g3 = QT + (int64_t)(a3 - l_min) * p * NxP;
-        double xs = 0.0;
-        for (int x = tid; x < Nx; x += NS2_THREADS) {
-            for (int c = 0; c < p; ++c) {
-                q1[c * NS2_THREADS + tid] = g1[c * NxP + x];
-                q2[c * NS2_THREADS + tid] = g2[c * NxP + x];
-                q3[c * NS2_THREADS + tid] = g3[c * NxP + x];
-            }
-            for (int b = 0, pr = 0; b < p; ++b) {
-                const double b2 = q2[b * NS2_THREADS + tid], b3 = q3[b * NS2_THREADS + tid];
-                for (int a = 0; a <= b; ++a, ++pr)
-                    S[pr * NS2_THREADS + tid] =
-                        q2[a * NS2_THREADS + tid] * b3 + b2 * q3[a * NS2_THREADS + tid];
-            }
-            double Bx = 0.0;
-            for (int m = 0; m < nm; ++m) {
-                const int* e = md + 6 * m;
-                const double f = q1[e[2] * NS2_THREADS + tid] * S[e[3] * NS2_THREADS + tid] +
-                                 q1[e[1] * NS2_THREADS + tid] * S[e[4] * NS2_THREADS + tid] +
-                                 q1[e[0] * NS2_THREADS + tid] * S[e[5] * NS2_THREADS + tid];
-                Bx += al[m] * f;
-            }
-            xs += wr2[x] * Bx;
-        }
-        for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
-        if (lane == 0) red[warp] = xs;
-        __syncthreads();
-        double X = 0.0;
-        for (int w = 0; w < NS2_THREADS / 32; ++w) X += red[w];
-        const double wz = W[t] * zm_weight(mode, a1, a2, a3, C, v, l_min, lf) * X;
-        for (int m = tid; m < nm; m += NS2_THREADS) {
-            const int i = md[6 * m], j = md[6 * m + 1], k = md[6 * m + 2];
-            const double* qi = q + (int64_t)i * L - l_min;
-            const double* qj = q + (int64_t)j * L - l_min;
-            const double* qk = q + (int64_t)k * L - l_min;
-            const double P = qi[a1] * (qj[a2] * qk[a3] + qk[a2] * qj[a3]) +
-                             qj[a1] * (qi[a2] * qk[a3] + qk[a2] * qi[a3]) +
-                             qk[a1] * (qi[a2] * qj[a3] + qj[a2] * qi[a3]);
-            b_acc[m] += wz * P;
-        }
-        __syncthreads();
-    }
-    for (int i = tid; i < nm; i += NS2_THREADS) partial[(int64_t)blockIdx.x * nm + i] = b_acc[i];
-}
-
-// Register-resident pointwise kernel for a compile-time basis size P (config 3: P = 8).
-// Per (triple, x): q̃(l1)[c] and the pair sums S_ab(x) live in registers; the mode sum walks
-// every ordered triple i <= j <= k < P with compile-time indices and a dense α table
-// (zero for triples absent from the mapping, read as shared-memory broadcasts):
-//   B(t,x) = Σ_{i<=j<=k} α_ijk [q̃_k(l1) S_ij + q̃_j(l1) S_ik + q̃_i(l1) S_jk]
+// Warp-per-triple pointwise kernel for a compile-time basis size P (<= MG_NS_PMAX).
+// Per (triple, x) — one lane per x — q̃ at l1, l2, l3 is loaded into registers and the
+// primordial bispectrum is summed pointwise over the mode set through the symmetric
+// coefficient table Ã (kernel parameter, i.e. constant-bank operands of the DFMAs):
+//   B(t,x) = Σ_c q̃_c(x,l1) Σ_{a<=b} Ã[c][ab] S_ab(x),   S_ab = q̃_a(l2)q̃_b(l3) + q̃_b(l2)q̃_a(l3)
+// with Ã[k][ij] += α_n, Ã[j][ik] += α_n, Ã[i][jk] += α_n for every mode n = (i<=j<=k) — the
+// same 3-term split of the 6-permutation product as f in engine3d.py:115-116, so the sum is
+// identical term by term (only its order changes).  The x integral is a warp butterfly; the
+// projection b[m] += W_t zm_t X_t P[m,t] is done by the same warp (lane m mod 32 owns mode m,
+// q at l1/l2/l3 exchanged by shuffles) into a per-warp shared-memory partial, reduced in warp
+// order at the end: one deterministic partial per CTA, no atomics.
 template <int P>
-__global__ void __launch_bounds__(128)
-k_nonsep_reg(const int32_t* __restrict__ t1, const int32_t* __restrict__ t2,
-             const int32_t* __restrict__ t3, const double* __restrict__ W, int64_t count,
-             const double* __restrict__ QT, const double* __restrict__ wr2,
-             const double* __restrict__ q, const double* __restrict__ C,
-             const double* __restrict__ v, const double* __restrict__ lf, int mode,
-             const double* __restrict__ alpha_dense, const int* __restrict__ modes, int nm,
-             int Nx, int NxP, int L, int l_min, double* __restrict__ partial) {
-    constexpr int NT = P * (P + 1) * (P + 2) / 6;
-    constexpr int P2 = P * (P + 1) / 2;
+struct NsAlpha {
+    double a[P][P * (P + 1) / 2];
+};
+
+constexpr int NSW_THREADS = 256;
+
+template <int P>
+__global__ void __launch_bounds__(NSW_THREADS, 1)
+k_nonsep_warp(const int4* __restrict__ trip, const double* __restrict__ W, int64_t count,
+              const double* __restrict__ QT, const double* __restrict__ wr2,
+              const double* __restrict__ q, const double* __restrict__ C,
+              const double* __restrict__ v, const double* __restrict__ lf, int mode,
+              const NsAlpha<P> al, const int* __restrict__ modes, int nm, int Nx, int NxP, int L,
+              int l_min, double* __restrict__ partial) {
+    constexpr int NW = NSW_THREADS / 32;
     extern __shared__ double sh[];
-    double* al = sh;                 // [NT] dense α in (k, j, i) order
-    double* b_acc = al + NT;         // [nm]
-    double* red = b_acc + nm;        // [4]
-    for (int i = threadIdx.x; i < NT; i += blockDim.x) al[i] = alpha_dense[i];
-    for (int i = threadIdx.x; i < nm; i += blockDim.x) b_acc[i] = 0.0;
-    __syncthreads();
+    double* bacc = sh;                                       // [NW][nm]
+    int* md = reinterpret_cast<int*>(bacc + (size_t)NW * nm);  // [nm][3]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int64_t t = blockIdx.x; t < count; t += gridDim.x) {
-        const int a1 = t1[t], a2 = t2[t], a3 = t3[t];
-        const double* g1 = QT + (int64_t)(a1 - l_min) * P * NxP;
-        const double* g2 = QT + (int64_t)(a2 - l_min) * P * NxP;
-        const double* g3 = QT + (int64_t)(a3 - l_min) * P * NxP;
+    for (int i = tid; i < NW * nm; i += NSW_THREADS) bacc[i] = 0.0;
+    for (int i = tid; i < 3 * nm; i += NSW_THREADS) md[i] = modes[i];
+    __syncthreads();
+    double* my = bacc + (size_t)warp * nm;
+    const int64_t nwarps = (int64_t)gridDim.x * NW;
+    for (int64_t t = (int64_t)blockIdx.x * NW + warp; t < count; t += nwarps) {
+        const int4 tr = trip[t];
+        const double* g1 = QT + (int64_t)(tr.x - l_min) * P * NxP;
+        const double* g2 = QT + (int64_t)(tr.y - l_min) * P * NxP;
+        const double* g3 = QT + (int64_t)(tr.z - l_min) * P * NxP;
         double xs = 0.0;
-        for (int x = tid; x < Nx; x += blockDim.x) {
-            double q1[P], q2[P], q3[P], S[P2];
+        // software pipeline: the next x column's 3P loads are in flight during this one's
+        // P(P+1)/2 (P + 2) DFMAs
+        double n1[P], n2[P], n3[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+            n1[c] = lane < Nx ? g1[c * NxP + lane] : 0.0;
+            n2[c] = lane < Nx ? g2[c * NxP + lane] : 0.0;
+            n3[c] = lane < Nx ? g3[c * NxP + lane] : 0.0;
+        }
+#pragma unroll 1
+        for (int x = lane; x < Nx; x += 32) {
+            double q1[P], q2[P], q3[P], T[P];
 #pragma unroll
             for (int c = 0; c < P; ++c) {
-                q1[c] = g1[c * NxP + x];
-                q2[c] = g2[c * NxP + x];
-                q3[c] = g3[c * NxP + x];
+                q1[c] = n1[c];
+                q2[c] = n2[c];
+                q3[c] = n3[c];
+                T[c] = 0.0;
+            }
+            if (x + 32 < Nx) {
+#pragma unroll
+                for (int c = 0; c < P; ++c) {
+                    n1[c] = g1[c * NxP + x + 32];
+                    n2[c] = g2[c * NxP + x + 32];
+                    n3[c] = g3[c * NxP + x + 32];
+                }
             }
 #pragma unroll
-            for (int b = 0; b < P; ++b)
+            for (int b = 0; b < P; ++b) {
 #pragma unroll
-                for (int a = 0; a <= b; ++a) S[b * (b + 1) / 2 + a] = q2[a] * q3[b] + q2[b] * q3[a];
-            double Bx = 0.0;
-            int n = 0;
+                for (int a = 0; a <= b; ++a) {
+                    const double s = q2[a] * q3[b] + q2[b] * q3[a];
 #pragma unroll
-            for (int k = 0; k < P; ++k)
+                    for (int c = 0; c < P; ++c) T[c] = fma(al.a[c][b * (b + 1) / 2 + a], s, T[c]);
+                }
+            }
+            double B = 0.0;
 #pragma unroll
-                for (int j = 0; j <= k; ++j)
-#pragma unroll
-                    for (int i = 0; i <= j; ++i, ++n) {
-                        const double f = q1[k] * S[j * (j + 1) / 2 + i] +
-                                         q1[j] * S[k * (k + 1) / 2 + i] +
-                                         q1[i] * S[k * (k + 1) / 2 + j];
-                        Bx += al[n] * f;
-                    }
-            xs += wr2[x] * Bx;
+            for (int c = 0; c < P; ++c) B = fma(q1[c], T[c], B);
+            xs = fma(wr2[x], B, xs);
         }
+#pragma unroll
         for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
-        if (lane == 0) red[warp] = xs;
-        __syncthreads();
-        const double X = red[0] + red[1] + red[2] + red[3];
-        const double wz = W[t] * zm_weight(mode, a1, a2, a3, C, v, l_min, lf) * X;
-        for (int m = tid; m < nm; m += blockDim.x) {
-            const int i = modes[3 * m], j = modes[3 * m + 1], k = modes[3 * m + 2];
-            const double* qi = q + (int64_t)i * L - l_min;
-            const double* qj = q + (int64_t)j * L - l_min;
-            const double* qk = q + (int64_t)k * L - l_min;
-            const double Pm = qi[a1] * (qj[a2] * qk[a3] + qk[a2] * qj[a3]) +
-                              qj[a1] * (qi[a2] * qk[a3] + qk[a2] * qi[a3]) +
-                              qk[a1] * (qi[a2] * qj[a3] + qj[a2] * qi[a3]);
-            b_acc[m] += wz * Pm;
+        const double wz = W[t] * zm_weight(mode, tr.x, tr.y, tr.z, C, v, l_min, lf) * xs;
+        // q_c at l1, l2, l3 in lane c (P <= 32), exchanged by shuffles per mode
+        double qa = 0.0, qb = 0.0, qc = 0.0;
+        if (lane < P) {
+            const double* ql = q + (int64_t)lane * L - l_min;
+            qa = ql[tr.x];
+            qb = ql[tr.y];
+            qc = ql[tr.z];
         }
-        __syncthreads();
+        for (int m0 = 0; m0 < nm; m0 += 32) {
+            const int m = m0 + lane;
+            const int i = m < nm ? md[3 * m] : 0, j = m < nm ? md[3 * m + 1] : 0,
+                      k = m < nm ? md[3 * m + 2] : 0;
+            const double i1 = __shfl_sync(0xffffffffu, qa, i), j1 = __shfl_sync(0xffffffffu, qa, j),
+                         k1 = __shfl_sync(0xffffffffu, qa, k);
+            const double i2 = __shfl_sync(0xffffffffu, qb, i), j2 = __shfl_sync(0xffffffffu, qb, j),
+                         k2 = __shfl_sync(0xffffffffu, qb, k);
+            const double i3 = __shfl_sync(0xffffffffu, qc, i), j3 = __shfl_sync(0xffffffffu, qc, j),
+                         k3 = __shfl_sync(0xffffffffu, qc, k);
+            const double Pm = i1 * (j2 * k3 + k2 * j3) + j1 * (i2 * k3 + k2 * i3) +
+                              k1 * (i2 * j3 + j2 * i3);
+            if (m < nm) my[m] += wz * Pm;
+        }
     }
-    for (int i = tid; i < nm; i += blockDim.x) partial[(int64_t)blockIdx.x * nm + i] = b_acc[i];
-}
-
-template <int P>
-static void launch_nonsep_reg(int nblocks, cudaStream_t st, const int32_t* d1, const int32_t* d2,
-                              const int32_t* d3, const double* dW, int64_t count, mg_plan* Pl,
-                              const double* alpha_dense, double* part) {
-    constexpr int NT = P * (P + 1) * (P + 2) / 6;
-    const size_t shm = (size_t)(NT + Pl->nm + 4) * sizeof(double);
-    k_nonsep_reg<P><<<nblocks, 128, shm, st>>>(d1, d2, d3, dW, count, Pl->QT.p, Pl->wr2.p,
-                                                Pl->q.p, Pl->C.p, Pl->v.p, Pl->lf.p, Pl->h2_mode,
-                                                alpha_dense, Pl->modes.p, Pl->nm, Pl->Nx,
-                                                Pl->NxP, Pl->L, Pl->l_min, part);
+    __syncthreads();
+    for (int m = tid; m < nm; m += NSW_THREADS) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += bacc[(size_t)w * nm + m];
+        partial[(int64_t)blockIdx.x * nm + m] = s;
+    }
 }
 
 __global__ void k_sum_partials(const double* __restrict__ partial, int nblocks, int nm,
@@ -1492,66 +1442,121 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int nblocks, 
     out[i] = s;
 }
 
-void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l2,
-            const int32_t* l3, const double* W, int64_t count, double* b, cudaStream_t st) {
-    const int nm = P->nm;
+template <int P>
+static void launch_nonsep_warp(mg_plan* Pl, const std::vector<double>& at, cudaStream_t st) {
+    NsAlpha<P> al;
+    constexpr int P2 = P * (P + 1) / 2;
+    for (int c = 0; c < P; ++c)
+        for (int ab = 0; ab < P2; ++ab) al.a[c][ab] = at[(size_t)c * P2 + ab];
+    const size_t shm = (size_t)(NSW_THREADS / 32) * Pl->nm * 8 + (size_t)3 * Pl->nm * 4;
+    static bool attr[64] = {false};
+    if (!attr[Pl->device & 63]) {
+        MG_CUDA(cudaFuncSetAttribute(k_nonsep_warp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     100 * 1024));
+        attr[Pl->device & 63] = true;
+    }
+    k_nonsep_warp<P><<<Pl->ns_blocks, NSW_THREADS, shm, st>>>(
+        reinterpret_cast<const int4*>(Pl->ns_trip.p), Pl->ns_W.p, Pl->ns_count, Pl->QT.p,
+        Pl->wr2.p, Pl->q.p, Pl->C.p, Pl->v.p, Pl->lf.p, Pl->h2_mode, al, Pl->modes.p, Pl->nm,
+        Pl->Nx, Pl->NxP, Pl->L, Pl->l_min, Pl->ns_part.p);
+}
+
+// Resident sparse domain of the non-separable path: validated, packed (l1,l2,l3,0) int4 + W.
+void nonsep_set_domain(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
+                       const double* W, int64_t count) {
+    std::vector<int32_t> packed(4 * (size_t)count);
     for (int64_t i = 0; i < count; ++i) {
         MG_REQUIRE(l1[i] <= l2[i] && l2[i] <= l3[i], "triples must satisfy l1 <= l2 <= l3");
         MG_REQUIRE(l1[i] >= P->l_min && l3[i] <= P->l_max, "triple outside [l_min, l_max]");
+        MG_REQUIRE(std::isfinite(W[i]), "sparse-domain weights must be finite");
+        packed[4 * i] = l1[i];
+        packed[4 * i + 1] = l2[i];
+        packed[4 * i + 2] = l3[i];
+        packed[4 * i + 3] = 0;
     }
-    DBuf<int32_t> d1, d2, d3;
-    DBuf<double> dW, dal, dout;
-    d1.upload(l1, count, st);
-    d2.upload(l2, count, st);
-    d3.upload(l3, count, st);
-    dW.upload(W, count, st);
-    dal.upload(alpha, nm, st);
-    const int nblocks = 148 * 8;
-    DBuf<double> part((size_t)nblocks * nm);
-    dout.alloc(nm);
-    const int p = P->p, P2 = p * (p + 1) / 2;
-    const size_t shm2 = (size_t)(3 * p + P2) * NS2_THREADS * 8 + 2 * (size_t)nm * 8 +
-                        NS2_THREADS / 32 * 8 + (size_t)6 * nm * 4;
-    // dense α over all ordered triples (k, j, i order), zero where the mapping has no mode
-    std::vector<double> ad((size_t)p * (p + 1) * (p + 2) / 6, 0.0);
-    {
-        std::vector<int> md(3 * (size_t)nm);
-        MG_CUDA(cudaMemcpy(md.data(), P->modes.p, md.size() * sizeof(int), cudaMemcpyDeviceToHost));
-        for (int m = 0; m < nm; ++m) {
-            const int i = md[3 * m], j = md[3 * m + 1], k = md[3 * m + 2];
-            ad[(size_t)k * (k + 1) * (k + 2) / 6 + j * (j + 1) / 2 + i] = alpha[m];
-        }
-    }
-    DBuf<double> dad;
-    dad.upload(ad.data(), ad.size(), st);
-    const bool reg = p == 4 || p == 6 || p == 8 || p == 10;
-    if (reg) {
-        switch (p) {
-            case 4: launch_nonsep_reg<4>(nblocks, st, d1.p, d2.p, d3.p, dW.p, count, P, dad.p, part.p); break;
-            case 6: launch_nonsep_reg<6>(nblocks, st, d1.p, d2.p, d3.p, dW.p, count, P, dad.p, part.p); break;
-            case 8: launch_nonsep_reg<8>(nblocks, st, d1.p, d2.p, d3.p, dW.p, count, P, dad.p, part.p); break;
-            default: launch_nonsep_reg<10>(nblocks, st, d1.p, d2.p, d3.p, dW.p, count, P, dad.p, part.p); break;
-        }
-    } else if (shm2 <= 200 * 1024) {
-        MG_CUDA(cudaFuncSetAttribute(k_nonsep2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)shm2));
-        k_nonsep2<<<nblocks, NS2_THREADS, shm2, st>>>(
-            d1.p, d2.p, d3.p, dW.p, count, P->QT.p, P->wr2.p, P->q.p, P->C.p, P->v.p, P->lf.p,
-            P->h2_mode, dal.p, P->modes.p, P->p, nm, P->Nx, P->NxP, P->L, P->l_min, part.p);
+    P->ns_count = count;
+    if (!count) return;
+    P->ns_trip.upload(packed.data(), packed.size());
+    P->ns_W.upload(W, count);
+    MG_CUDA(cudaStreamSynchronize(0));  // packed is pageable host memory
+}
+
+// b = Σ_t W_t zm_t P[:,t] Σ_x wr2_x B(t,x) over the resident sparse domain; b_dev (device,
+// optional) and b_host (optional) receive the nm coefficients.
+void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_host,
+                    cudaStream_t st) {
+    const int nm = P->nm, p = P->p, P2 = P->P2;
+    P->ns_b.ensure(nm);
+    if (P->ns_count == 0) {
+        MG_CUDA(cudaMemsetAsync(P->ns_b.p, 0, nm * sizeof(double), st));
     } else {
-        size_t shm = (size_t)nm * 8 + NS_THREADS / 32 * 8 + (3 * nm + 1) * 4 + 8 + (size_t)nm * 8;
-        if (shm > 48 * 1024)
-            MG_CUDA(cudaFuncSetAttribute(k_nonsep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)shm));
-        k_nonsep<<<nblocks, NS_THREADS, shm, st>>>(
-            d1.p, d2.p, d3.p, dW.p, count, P->QT.p, P->wr2.p, P->q.p, P->C.p, P->v.p, P->lf.p,
-            P->h2_mode, dal.p, P->modes.p, P->p, nm, P->Nx, P->NxP, P->L, P->l_min, part.p);
+        // symmetric coefficient table Ã[c][ab] (see k_nonsep_warp), host-built per call
+        std::vector<double> at((size_t)p * P2, 0.0);
+        for (int m = 0; m < nm; ++m) {
+            const int i = P->hmodes[3 * m], j = P->hmodes[3 * m + 1], k = P->hmodes[3 * m + 2];
+            at[(size_t)k * P2 + pair_idx(i, j)] += alpha[m];
+            at[(size_t)j * P2 + pair_idx(i, k)] += alpha[m];
+            at[(size_t)i * P2 + pair_idx(j, k)] += alpha[m];
+        }
+        if (!P->ns_blocks) {
+            int sms = 148;
+            MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
+            P->ns_blocks = 2 * sms;
+        }
+        P->ns_part.ensure((size_t)P->ns_blocks * nm);
+        MG_REQUIRE((size_t)(NSW_THREADS / 32) * nm * 8 + (size_t)3 * nm * 4 <= 100 * 1024,
+                   "too many modes for the non-separable kernel");
+        if (P->profile) {
+            if (!P->ns_ev[0]) {
+                MG_CUDA(cudaEventCreate(&P->ns_ev[0]));
+                MG_CUDA(cudaEventCreate(&P->ns_ev[1]));
+            }
+            MG_CUDA(cudaEventRecord(P->ns_ev[0], st));
+        }
+        switch (p) {
+#define MG_NS_CASE(N) \
+    case N: launch_nonsep_warp<N>(P, at, st); break;
+            MG_NS_CASE(1) MG_NS_CASE(2) MG_NS_CASE(3) MG_NS_CASE(4) MG_NS_CASE(5) MG_NS_CASE(6)
+            MG_NS_CASE(7) MG_NS_CASE(8) MG_NS_CASE(9) MG_NS_CASE(10) MG_NS_CASE(11)
+            MG_NS_CASE(12) MG_NS_CASE(13) MG_NS_CASE(14) MG_NS_CASE(15) MG_NS_CASE(16)
+#undef MG_NS_CASE
+            default: {
+                P->ns_alpha.upload(alpha, nm, st);
+                const size_t shm = (size_t)nm * 8 + NS_THREADS / 32 * 8 + (3 * nm + 1) * 4 + 8 +
+                                   (size_t)nm * 8;
+                MG_CUDA(cudaFuncSetAttribute(k_nonsep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)std::max<size_t>(shm, 48 * 1024)));
+                k_nonsep<<<P->ns_blocks, NS_THREADS, shm, st>>>(
+                    reinterpret_cast<const int4*>(P->ns_trip.p), P->ns_W.p, P->ns_count, P->QT.p,
+                    P->wr2.p, P->q.p, P->C.p, P->v.p, P->lf.p, P->h2_mode, P->ns_alpha.p, P->modes.p, p,
+                    nm, P->Nx, P->NxP, P->L, P->l_min, P->ns_part.p);
+                break;
+            }
+        }
+        MG_LAUNCHED();
+        k_sum_partials<<<(nm + 127) / 128, 128, 0, st>>>(P->ns_part.p, P->ns_blocks, nm, P->ns_b.p);
+        MG_LAUNCHED();
+        if (P->profile) {
+            MG_CUDA(cudaEventRecord(P->ns_ev[1], st));
+            MG_CUDA(cudaEventSynchronize(P->ns_ev[1]));
+            float ms = 0.f;
+            MG_CUDA(cudaEventElapsedTime(&ms, P->ns_ev[0], P->ns_ev[1]));
+            P->prof_ms[7] += ms;
+        }
+        P->launches = 2;
     }
-    MG_LAUNCHED();
-    k_sum_partials<<<(nm + 127) / 128, 128, 0, st>>>(part.p, nblocks, nm, dout.p);
-    MG_LAUNCHED();
-    MG_CUDA(cudaMemcpyAsync(b, dout.p, nm * sizeof(double), cudaMemcpyDeviceToHost, st));
-    MG_CUDA(cudaStreamSynchronize(st));
+    if (b_dev)
+        MG_CUDA(cudaMemcpyAsync(b_dev, P->ns_b.p, nm * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (b_host) {
+        MG_CUDA(cudaMemcpyAsync(b_host, P->ns_b.p, nm * sizeof(double), cudaMemcpyDeviceToHost, st));
+        MG_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
+void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l2,
+            const int32_t* l3, const double* W, int64_t count, double* b, cudaStream_t st) {
+    nonsep_set_domain(P, l1, l2, l3, W, count);
+    nonsep_execute(P, alpha, nullptr, b, st);
 }
 
 }  // namespace mg

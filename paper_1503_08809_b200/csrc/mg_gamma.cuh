@@ -20,7 +20,7 @@ struct MgTile {
     int row0, c0, nslots, nrows, jlo, jhi, pad0, pad1;
 };
 
-constexpr int MG_NPROF = 7;
+constexpr int MG_NPROF = 8;
 
 // Batch scratch, pooled per device so that one-shot calls (the drop-in API) do not pay for
 // allocating and zeroing gigabytes every time.  Buffers only grow; they are zeroed when
@@ -70,7 +70,7 @@ struct mg_plan {
     // optional kernel timing: ms per family {exposed operand wait, run, x, gather, pair,
     // final, side-stream operand kernels (overlapped)}
     bool profile = false;
-    double prof_ms[MG_NPROF] = {0, 0, 0, 0, 0, 0, 0};
+    double prof_ms[MG_NPROF] = {0, 0, 0, 0, 0, 0, 0, 0};
     std::vector<cudaEvent_t> prof_events;
     std::vector<int> prof_tags;
     size_t prof_used = 0;
@@ -85,13 +85,20 @@ struct mg_plan {
         for (auto e : prof_events) cudaEventDestroy(e);
         for (auto e : side_events) cudaEventDestroy(e);
         for (cudaEvent_t e : {ev_start[0], ev_start[1], ev_end[0], ev_end[1], ev_panel[0],
-                              ev_panel[1], ev_s, ev_x})
+                              ev_panel[1], ev_s, ev_x, ns_ev[0], ns_ev[1]})
             if (e) cudaEventDestroy(e);
         if (ms) cudaStreamDestroy(ms);
         if (ss) cudaStreamDestroy(ss);
     }
     // host copies (for the direct/nonsep paths)
     std::vector<double> hC, hv;
+    std::vector<int> hmodes;  // [nm][3]
+    // resident sparse domain + buffers of the non-separable path
+    mg::DBuf<int32_t> ns_trip;  // [count][4] = l1, l2, l3, 0
+    mg::DBuf<double> ns_W, ns_part, ns_b, ns_alpha;
+    int64_t ns_count = 0;
+    int ns_blocks = 0;
+    cudaEvent_t ns_ev[2] = {};
 };
 
 namespace mg {
@@ -106,6 +113,10 @@ void execute_rows(mg_plan* P, const std::vector<MgRow>& rows, cudaStream_t st);
 void execute_slab(mg_plan* P, int l2a, int l2b, cudaStream_t st);
 void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
                      int64_t count, cudaStream_t st);
+void nonsep_set_domain(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
+                       const double* W, int64_t count);
+void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_host,
+                    cudaStream_t st);
 void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l2,
             const int32_t* l3, const double* W, int64_t count, double* b, cudaStream_t st);
 void weights(int l_min, int l_max, const double* C, const double* v, int h2_mode,

@@ -76,10 +76,35 @@ class GammaPlan:
         nat.check(nat.lib().mg_plan_set_profile(self._h, int(bool(on))))
 
     def kernel_ms(self) -> dict:
-        ms = np.zeros(7)
+        ms = np.zeros(8)
         nat.check(nat.lib().mg_plan_kernel_ms(self._h, nat.ptr(ms)))
-        return dict(zip(("operands", "run", "x", "gather", "pair", "final", "operands_side"),
-                        ms.tolist()))
+        return dict(zip(("operands", "run", "x", "gather", "pair", "final", "operands_side",
+                         "nonsep"), ms.tolist()))
+
+    # ---- non-separable path on a resident sparse domain (BASELINE config 3) ----
+    def set_sparse_domain(self, domain):
+        """Upload a `SparseDomain` (l1, l2, l3, weight) once for repeated `nonsep` calls."""
+        self._ns = tuple(np.ascontiguousarray(a, np.int32) for a in (domain.l1, domain.l2,
+                                                                      domain.l3))
+        W = np.ascontiguousarray(domain.weight, np.float64)
+        nat.check(nat.lib().mg_plan_set_sparse_domain(self._h, *(nat.ptr(a) for a in self._ns),
+                                                      nat.ptr(W), int(W.size)))
+
+    def nonsep(self, alpha, out=None, stream=None) -> np.ndarray | None:
+        """b = Σ_t W_t zm_t P[:,t] Σ_x wr2_x B(t,x) for primordial coefficients `alpha` [n].
+        With `out` (CUDA torch tensor [n]) the result stays on the device (asynchronous);
+        otherwise it is returned as a host array."""
+        a = np.ascontiguousarray(alpha, np.float64)
+        if a.shape != (self.n,):
+            raise ValueError("alpha must have one coefficient per primordial mode")
+        s = None if stream is None else ctypes.c_void_p(stream.cuda_stream)
+        if out is not None:
+            nat.check(nat.lib().mg_plan_nonsep(self._h, nat.ptr(a),
+                                               ctypes.c_void_p(out.data_ptr()), None, s))
+            return None
+        b = np.zeros(self.n)
+        nat.check(nat.lib().mg_plan_nonsep(self._h, nat.ptr(a), None, nat.ptr(b), s))
+        return b
 
     def close(self):
         if self._h:

@@ -100,3 +100,75 @@ class TestNonSeparable:
                                  l3, W)
         assert b.shape == (120, 1)
         assert np.linalg.norm(b.values[:, 0] - want) <= 1e-8 * np.linalg.norm(want)
+
+    @staticmethod
+    def _small(p, l_max=120, seed=11, nx=40):
+        """Random tables of basis size p on a small sparse grid (kernel-shape coverage)."""
+        from paper_1503_08809_b200.basis import default_mode_mapping
+        rng = np.random.default_rng(seed)
+        L = l_max - 1
+        q = rng.standard_normal((p, L))
+        qt = rng.standard_normal((p, nx, L)) * 1e-3
+        C = rng.uniform(0.5, 2.0, L)
+        v = (2.0 * np.arange(2, l_max + 1) + 1.0) ** (1.0 / 6.0)
+        x = np.linspace(13600.0, 14400.0, nx)
+        entries = default_mode_mapping(p).entries
+        grid, w = sparse_grid(l_max=l_max, dense_to=30, step=7)
+        dom = SparseDomain(*sparse_domain(grid, w))
+        alpha = rng.standard_normal(entries.shape[0])
+        return q, qt, C, v, x, entries, dom, alpha
+
+    @pytest.mark.parametrize("p", [1, 3, 5, 8, 12, 16, 18])
+    def test_basis_sizes_against_restatement(self, p):
+        """Every compile-time kernel instance (p <= 16) and the generic kernel (p > 16)."""
+        from paper_1503_08809_b200.quadrature import x_weights
+        q, qt, C, v, x, entries, dom, alpha = self._small(p, nx=37 if p % 2 else 40)
+        t = BasisTables(q, qt, C, v, 2, q.shape[1] + 1)
+        m = ModeMapping(entries, p)
+        b = gamma_nonsep(t, m, RadialGrid(x), alpha, dom).values[:, 0]
+        want = nonsep_ref.nonsep(q, qt, C, v, x_weights(x, "trap"), entries, alpha, 2,
+                                 dom.l1, dom.l2, dom.l3, dom.weight)
+        assert np.linalg.norm(b - want) <= 1e-8 * np.linalg.norm(want)
+
+    def test_mode_subset(self):
+        """A mapping with a subset of the ordered triples (Ã built only from its modes)."""
+        from paper_1503_08809_b200.quadrature import x_weights
+        q, qt, C, v, x, entries, dom, alpha = self._small(6)
+        keep = np.arange(0, entries.shape[0], 3)
+        ent, al = entries[keep], alpha[keep]
+        t = BasisTables(q, qt, C, v, 2, q.shape[1] + 1)
+        b = gamma_nonsep(t, ModeMapping(ent, 6), RadialGrid(x), al, dom).values[:, 0]
+        want = nonsep_ref.nonsep(q, qt, C, v, x_weights(x, "trap"), ent, al, 2, dom.l1, dom.l2,
+                                 dom.l3, dom.weight)
+        assert b.shape == (keep.size,)
+        assert np.linalg.norm(b - want) <= 1e-8 * np.linalg.norm(want)
+
+    def test_resident_plan(self):
+        """GammaPlan.set_sparse_domain/nonsep: same b as the one-shot call, bitwise stable
+        across calls, linear in α, device output, empty domain -> zeros."""
+        import torch
+        from paper_1503_08809_b200 import GammaPlan
+        from paper_1503_08809_b200.quadrature import x_weights
+        q, qt, C, v, x, entries, dom, alpha = self._small(8)
+        lmax = q.shape[1] + 1
+        t = BasisTables(q, qt, C, v, 2, lmax)
+        one = gamma_nonsep(t, ModeMapping(entries, 8), RadialGrid(x), alpha, dom).values[:, 0]
+        plan = GammaPlan(q, qt, C, v, x_weights(x, "trap"), entries, 2, lmax)
+        plan.set_sparse_domain(dom)
+        b1 = plan.nonsep(alpha)
+        b2 = plan.nonsep(alpha)
+        assert np.array_equal(b1, b2)
+        assert np.array_equal(b1, one)
+        b3 = plan.nonsep(2.0 * alpha - 0.5 * alpha)   # linear in α
+        assert np.linalg.norm(b3 - 1.5 * b1) <= 1e-13 * np.linalg.norm(b1)
+        out = torch.zeros(entries.shape[0], dtype=torch.float64, device="cuda")
+        plan.nonsep(alpha, out=out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), b1)
+        plan.set_sparse_domain(SparseDomain([], [], [], []))
+        assert not plan.nonsep(alpha).any()
+        with pytest.raises(ValueError):
+            plan.nonsep(alpha[:-1])
+        with pytest.raises(ValueError):
+            plan.set_sparse_domain(SparseDomain([5], [3], [4], [1.0]))
+        plan.close()
