@@ -209,12 +209,15 @@ int mg_plan_set_profile(mg_plan* P, int on) {
         MG_REQUIRE(P, "null plan");
         P->profile = on != 0;
         for (double& m : P->prof_ms) m = 0.0;
+        P->ns_used = 0;
     });
 }
 
 int mg_plan_kernel_ms(mg_plan* P, double* ms) {
     return guarded([&] {
         MG_REQUIRE(P && ms, "null argument");
+        DeviceGuard g(P->device);
+        nonsep_collect(P);
         for (int i = 0; i < MG_NPROF; ++i) ms[i] = P->prof_ms[i];
     });
 }

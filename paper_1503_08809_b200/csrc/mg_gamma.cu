@@ -1332,7 +1332,13 @@ struct NsAlpha {
     double a[P][P * (P + 1) / 2];
 };
 
-constexpr int NSW_THREADS = 256;
+#ifndef NSW_THREADS_
+#define NSW_THREADS_ 128  // 168 registers: 3 CTAs (12 warps) per SM
+#endif
+constexpr int NSW_THREADS = NSW_THREADS_;
+#ifndef NS_XV
+#define NS_XV 1  // x columns per lane in k_nonsep_warp (2 and 3 measured slower)
+#endif
 
 template <int P>
 __global__ void __launch_bounds__(NSW_THREADS, 1)
@@ -1358,46 +1364,46 @@ k_nonsep_warp(const int4* __restrict__ trip, const double* __restrict__ W, int64
         const double* g2 = QT + (int64_t)(tr.y - l_min) * P * NxP;
         const double* g3 = QT + (int64_t)(tr.z - l_min) * P * NxP;
         double xs = 0.0;
-        // software pipeline: the next x column's 3P loads are in flight during this one's
-        // P(P+1)/2 (P + 2) DFMAs
-        double n1[P], n2[P], n3[P];
-#pragma unroll
-        for (int c = 0; c < P; ++c) {
-            n1[c] = lane < Nx ? g1[c * NxP + lane] : 0.0;
-            n2[c] = lane < Nx ? g2[c * NxP + lane] : 0.0;
-            n3[c] = lane < Nx ? g3[c * NxP + lane] : 0.0;
-        }
+        // XV x columns per lane: every coefficient Ã[c][ab] (a uniform-register load) feeds
+        // XV DFMAs, and the XV independent accumulator sets double the ILP
 #pragma unroll 1
-        for (int x = lane; x < Nx; x += 32) {
-            double q1[P], q2[P], q3[P], T[P];
+        for (int x0 = lane; x0 < Nx; x0 += 32 * NS_XV) {
+            double q1[NS_XV][P], q2[NS_XV][P], q3[NS_XV][P], T[NS_XV][P];
 #pragma unroll
-            for (int c = 0; c < P; ++c) {
-                q1[c] = n1[c];
-                q2[c] = n2[c];
-                q3[c] = n3[c];
-                T[c] = 0.0;
-            }
-            if (x + 32 < Nx) {
+            for (int u = 0; u < NS_XV; ++u) {
+                const int x = x0 + 32 * u;
+                const bool ok = x < Nx;
 #pragma unroll
                 for (int c = 0; c < P; ++c) {
-                    n1[c] = g1[c * NxP + x + 32];
-                    n2[c] = g2[c * NxP + x + 32];
-                    n3[c] = g3[c * NxP + x + 32];
+                    q1[u][c] = ok ? g1[c * NxP + x] : 0.0;
+                    q2[u][c] = ok ? g2[c * NxP + x] : 0.0;
+                    q3[u][c] = ok ? g3[c * NxP + x] : 0.0;
+                    T[u][c] = 0.0;
                 }
             }
 #pragma unroll
             for (int b = 0; b < P; ++b) {
 #pragma unroll
                 for (int a = 0; a <= b; ++a) {
-                    const double s = q2[a] * q3[b] + q2[b] * q3[a];
+                    double sv[NS_XV];
 #pragma unroll
-                    for (int c = 0; c < P; ++c) T[c] = fma(al.a[c][b * (b + 1) / 2 + a], s, T[c]);
+                    for (int u = 0; u < NS_XV; ++u) sv[u] = q2[u][a] * q3[u][b] + q2[u][b] * q3[u][a];
+#pragma unroll
+                    for (int c = 0; c < P; ++c) {
+                        const double coef = al.a[c][b * (b + 1) / 2 + a];
+#pragma unroll
+                        for (int u = 0; u < NS_XV; ++u) T[u][c] = fma(coef, sv[u], T[u][c]);
+                    }
                 }
             }
-            double B = 0.0;
 #pragma unroll
-            for (int c = 0; c < P; ++c) B = fma(q1[c], T[c], B);
-            xs = fma(wr2[x], B, xs);
+            for (int u = 0; u < NS_XV; ++u) {
+                const int x = x0 + 32 * u;
+                double B = 0.0;
+#pragma unroll
+                for (int c = 0; c < P; ++c) B = fma(q1[u][c], T[u][c], B);
+                if (x < Nx) xs = fma(wr2[x], B, xs);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
@@ -1449,16 +1455,45 @@ static void launch_nonsep_warp(mg_plan* Pl, const std::vector<double>& at, cudaS
     for (int c = 0; c < P; ++c)
         for (int ab = 0; ab < P2; ++ab) al.a[c][ab] = at[(size_t)c * P2 + ab];
     const size_t shm = (size_t)(NSW_THREADS / 32) * Pl->nm * 8 + (size_t)3 * Pl->nm * 4;
-    static bool attr[64] = {false};
-    if (!attr[Pl->device & 63]) {
+    static int resident[64] = {0};  // CTAs per SM of this instance (per device)
+    int& res = resident[Pl->device & 63];
+    if (!res) {
         MG_CUDA(cudaFuncSetAttribute(k_nonsep_warp<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      100 * 1024));
-        attr[Pl->device & 63] = true;
+        MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_nonsep_warp<P>, NSW_THREADS,
+                                                              shm));
+        res = std::max(res, 1);
     }
+    int sms = 148;
+    MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, Pl->device));
+    Pl->ns_blocks = sms * res;
+    Pl->ns_part.ensure((size_t)Pl->ns_blocks * Pl->nm);
     k_nonsep_warp<P><<<Pl->ns_blocks, NSW_THREADS, shm, st>>>(
         reinterpret_cast<const int4*>(Pl->ns_trip.p), Pl->ns_W.p, Pl->ns_count, Pl->QT.p,
         Pl->wr2.p, Pl->q.p, Pl->C.p, Pl->v.p, Pl->lf.p, Pl->h2_mode, al, Pl->modes.p, Pl->nm,
         Pl->Nx, Pl->NxP, Pl->L, Pl->l_min, Pl->ns_part.p);
+}
+
+// Kernel timing of the non-separable path without a host synchronisation per call: event
+// pairs accumulate and are resolved when the timings are read (mg_plan_kernel_ms).
+static void ns_mark(mg_plan* P, cudaStream_t st) {
+    if (!P->profile) return;
+    if (P->ns_used == P->ns_events.size()) {
+        cudaEvent_t e;
+        MG_CUDA(cudaEventCreate(&e));
+        P->ns_events.push_back(e);
+    }
+    MG_CUDA(cudaEventRecord(P->ns_events[P->ns_used++], st));
+}
+
+void nonsep_collect(mg_plan* P) {
+    for (size_t i = 0; i + 1 < P->ns_used; i += 2) {
+        MG_CUDA(cudaEventSynchronize(P->ns_events[i + 1]));
+        float ms = 0.f;
+        MG_CUDA(cudaEventElapsedTime(&ms, P->ns_events[i], P->ns_events[i + 1]));
+        P->prof_ms[7] += ms;
+    }
+    P->ns_used = 0;
 }
 
 // Resident sparse domain of the non-separable path: validated, packed (l1,l2,l3,0) int4 + W.
@@ -1498,7 +1533,7 @@ void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_ho
             at[(size_t)j * P2 + pair_idx(i, k)] += alpha[m];
             at[(size_t)i * P2 + pair_idx(j, k)] += alpha[m];
         }
-        if (!P->ns_blocks) {
+        if (!P->ns_blocks || p > 16) {  // generic kernel (p > 16): 2 CTAs per SM
             int sms = 148;
             MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
             P->ns_blocks = 2 * sms;
@@ -1506,13 +1541,7 @@ void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_ho
         P->ns_part.ensure((size_t)P->ns_blocks * nm);
         MG_REQUIRE((size_t)(NSW_THREADS / 32) * nm * 8 + (size_t)3 * nm * 4 <= 100 * 1024,
                    "too many modes for the non-separable kernel");
-        if (P->profile) {
-            if (!P->ns_ev[0]) {
-                MG_CUDA(cudaEventCreate(&P->ns_ev[0]));
-                MG_CUDA(cudaEventCreate(&P->ns_ev[1]));
-            }
-            MG_CUDA(cudaEventRecord(P->ns_ev[0], st));
-        }
+        ns_mark(P, st);  // (start, end) event pair, resolved lazily by nonsep_collect
         switch (p) {
 #define MG_NS_CASE(N) \
     case N: launch_nonsep_warp<N>(P, at, st); break;
@@ -1536,13 +1565,7 @@ void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_ho
         MG_LAUNCHED();
         k_sum_partials<<<(nm + 127) / 128, 128, 0, st>>>(P->ns_part.p, P->ns_blocks, nm, P->ns_b.p);
         MG_LAUNCHED();
-        if (P->profile) {
-            MG_CUDA(cudaEventRecord(P->ns_ev[1], st));
-            MG_CUDA(cudaEventSynchronize(P->ns_ev[1]));
-            float ms = 0.f;
-            MG_CUDA(cudaEventElapsedTime(&ms, P->ns_ev[0], P->ns_ev[1]));
-            P->prof_ms[7] += ms;
-        }
+        ns_mark(P, st);
         P->launches = 2;
     }
     if (b_dev)

@@ -84,8 +84,9 @@ struct mg_plan {
     ~mg_plan() {
         for (auto e : prof_events) cudaEventDestroy(e);
         for (auto e : side_events) cudaEventDestroy(e);
+        for (auto e : ns_events) cudaEventDestroy(e);
         for (cudaEvent_t e : {ev_start[0], ev_start[1], ev_end[0], ev_end[1], ev_panel[0],
-                              ev_panel[1], ev_s, ev_x, ns_ev[0], ns_ev[1]})
+                              ev_panel[1], ev_s, ev_x})
             if (e) cudaEventDestroy(e);
         if (ms) cudaStreamDestroy(ms);
         if (ss) cudaStreamDestroy(ss);
@@ -98,7 +99,8 @@ struct mg_plan {
     mg::DBuf<double> ns_W, ns_part, ns_b, ns_alpha;
     int64_t ns_count = 0;
     int ns_blocks = 0;
-    cudaEvent_t ns_ev[2] = {};
+    std::vector<cudaEvent_t> ns_events;  // (start, end) pairs of profiled nonsep calls
+    size_t ns_used = 0;
 };
 
 namespace mg {
@@ -117,6 +119,7 @@ void nonsep_set_domain(mg_plan* P, const int32_t* l1, const int32_t* l2, const i
                        const double* W, int64_t count);
 void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_host,
                     cudaStream_t st);
+void nonsep_collect(mg_plan* P);
 void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l2,
             const int32_t* l3, const double* W, int64_t count, double* b, cudaStream_t st);
 void weights(int l_min, int l_max, const double* C, const double* v, int h2_mode,
