@@ -1327,6 +1327,34 @@ k_nonsep(const int4* __restrict__ trip, const double* __restrict__ W, int64_t co
 // projection b[m] += W_t zm_t X_t P[m,t] is done by the same warp (lane m mod 32 owns mode m,
 // q at l1/l2/l3 exchanged by shuffles) into a per-warp shared-memory partial, reduced in warp
 // order at the end: one deterministic partial per CTA, no atomics.
+// Projection of one triple onto the late-time modes by one warp: my[m] += wz P[m,t], lane =
+// mode (mod 32), q_c at l1/l2/l3 held by lane c (P <= 32) and exchanged by shuffles.
+__device__ __forceinline__ void ns_project(const int4 tr, double wz, const double* __restrict__ q,
+                                           const int* md, int P, int nm, int L, int l_min,
+                                           int lane, double* my) {
+    double qa = 0.0, qb = 0.0, qc = 0.0;
+    if (lane < P) {
+        const double* ql = q + (int64_t)lane * L - l_min;
+        qa = ql[tr.x];
+        qb = ql[tr.y];
+        qc = ql[tr.z];
+    }
+    for (int m0 = 0; m0 < nm; m0 += 32) {
+        const int m = m0 + lane;
+        const int i = m < nm ? md[3 * m] : 0, j = m < nm ? md[3 * m + 1] : 0,
+                  k = m < nm ? md[3 * m + 2] : 0;
+        const double i1 = __shfl_sync(0xffffffffu, qa, i), j1 = __shfl_sync(0xffffffffu, qa, j),
+                     k1 = __shfl_sync(0xffffffffu, qa, k);
+        const double i2 = __shfl_sync(0xffffffffu, qb, i), j2 = __shfl_sync(0xffffffffu, qb, j),
+                     k2 = __shfl_sync(0xffffffffu, qb, k);
+        const double i3 = __shfl_sync(0xffffffffu, qc, i), j3 = __shfl_sync(0xffffffffu, qc, j),
+                     k3 = __shfl_sync(0xffffffffu, qc, k);
+        const double Pm = i1 * (j2 * k3 + k2 * j3) + j1 * (i2 * k3 + k2 * i3) +
+                          k1 * (i2 * j3 + j2 * i3);
+        if (m < nm) my[m] += wz * Pm;
+    }
+}
+
 template <int P>
 struct NsAlpha {
     double a[P][P * (P + 1) / 2];
@@ -1408,28 +1436,7 @@ k_nonsep_warp(const int4* __restrict__ trip, const double* __restrict__ W, int64
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
         const double wz = W[t] * zm_weight(mode, tr.x, tr.y, tr.z, C, v, l_min, lf) * xs;
-        // q_c at l1, l2, l3 in lane c (P <= 32), exchanged by shuffles per mode
-        double qa = 0.0, qb = 0.0, qc = 0.0;
-        if (lane < P) {
-            const double* ql = q + (int64_t)lane * L - l_min;
-            qa = ql[tr.x];
-            qb = ql[tr.y];
-            qc = ql[tr.z];
-        }
-        for (int m0 = 0; m0 < nm; m0 += 32) {
-            const int m = m0 + lane;
-            const int i = m < nm ? md[3 * m] : 0, j = m < nm ? md[3 * m + 1] : 0,
-                      k = m < nm ? md[3 * m + 2] : 0;
-            const double i1 = __shfl_sync(0xffffffffu, qa, i), j1 = __shfl_sync(0xffffffffu, qa, j),
-                         k1 = __shfl_sync(0xffffffffu, qa, k);
-            const double i2 = __shfl_sync(0xffffffffu, qb, i), j2 = __shfl_sync(0xffffffffu, qb, j),
-                         k2 = __shfl_sync(0xffffffffu, qb, k);
-            const double i3 = __shfl_sync(0xffffffffu, qc, i), j3 = __shfl_sync(0xffffffffu, qc, j),
-                         k3 = __shfl_sync(0xffffffffu, qc, k);
-            const double Pm = i1 * (j2 * k3 + k2 * j3) + j1 * (i2 * k3 + k2 * i3) +
-                              k1 * (i2 * j3 + j2 * i3);
-            if (m < nm) my[m] += wz * Pm;
-        }
+        ns_project(tr, wz, q, md, P, nm, L, l_min, lane, my);
     }
     __syncthreads();
     for (int m = tid; m < nm; m += NSW_THREADS) {

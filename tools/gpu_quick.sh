@@ -1,6 +1,8 @@
 mkdir -p gpurun_out
-for v in default smemal smemal_t256 smemal_xv2; do
-  if [ $v = default ]; then unset MG_LIB_PATH; else export MG_LIB_PATH=$PWD/paper_1503_08809_b200/_native/variants/$v.so; fi
-  echo "== $v"; timeout 200 python bench.py --config c3 --steps 20 --warmup 2 --e2e-reps 1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['roofline']['kernel_ms_per_step'], d['roofline']['frac'], d['e2e']['matches_device_result'], d['b_norm'])"
+for v in prev t64bk32 t64bk16 prev t64bk32 t64bk16; do
+  export MG_LIB_PATH=$PWD/paper_1503_08809_b200/_native/variants/$v.so
+  for sl in "300 420" "1500 1540"; do
+    echo "== $v slab $sl"; timeout 200 python tools/time_slab.py --config c1 --l2 $sl --reps 3 2>&1 | tail -1
+  done
 done > gpurun_out/var.log 2>&1
 cat gpurun_out/var.log
