@@ -17,4 +17,11 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 300 python tools/prof_gamma.py > gpurun_out/prof_plain.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_(run|x|pair)_contract" -s 3 -c 3 \
       -o gpurun_out/prof_full python tools/prof_gamma.py > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_nonsep_warp -c 1 \
+      -o gpurun_out/prof_nonsep python bench.py --config c3 --steps 1 --warmup 1 > gpurun_out/ncu_nonsep.log 2>&1; echo "ncu nonsep rc=$?"
 fi
+# multi-rank path on one GPU (gloo exchange; the real run uses NCCL, one GPU per rank)
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 \
+    bench.py --gpus 2 --steps 2 --warmup 1 --dist-backend gloo --e2e-reps 1 > gpurun_out/bench_2rank_gloo.json 2> gpurun_out/bench_2rank.err; echo "2-rank rc=$?"
+# config 4 (p = 30) on one slab, extrapolated with the cost model
+timeout 600 python tools/time_slab.py --config c4 --l2 1500 1530 --reps 2 > gpurun_out/c4_slab.log 2>&1; echo "c4 rc=$?"; tail -2 gpurun_out/c4_slab.log
