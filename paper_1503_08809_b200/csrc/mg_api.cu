@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <functional>
+#include <future>
 #include <string>
 #include <vector>
 
@@ -271,16 +272,22 @@ int mg_gamma_sep(const double* q, const double* qt, const double* C, const doubl
                  int l_max, int h2_mode, int64_t begin, int64_t end, int device,
                  double* gamma) {
     return guarded([&] {
+        MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
+        // The rows of the flat range are enumerated on a host thread while the plan uploads
+        // and transposes q̃ (the one-shot drop-in call pays both every time).
+        std::vector<MgRow> rows;
+        auto host_rows = std::async(std::launch::async, [&] {
+            DomainIndex D;
+            D.build(l_min, l_max);
+            const int64_t e_ = end < 0 ? D.count : end;
+            int s[3], e[3];
+            full_range_bounds(D, begin, e_, s, e);
+            if (begin < e_) build_rows_range(l_min, l_max, l_min, l_max + 1, s, e, rows);
+        });
         gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, device, gamma,
                      [&](mg_plan* P) {
-                         DomainIndex D;
-                         D.build(l_min, l_max);
-                         int64_t e_ = end < 0 ? D.count : end;
-                         int s[3], e[3];
-                         full_range_bounds(D, begin, e_, s, e);
-                         std::vector<MgRow> rows;
-                         if (begin < e_) build_rows(P, l_min, l_max + 1, s, e, rows);
-                         execute_rows(P, rows, 0);
+                         host_rows.get();  // rethrows a range error from the host thread
+                         execute_rows(P, std::move(rows), 0);
                      });
     });
 }

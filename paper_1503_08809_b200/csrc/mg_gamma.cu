@@ -638,7 +638,10 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
                                   make_longlong2(P->wbase[0], P->wbase[1]),
                                   make_int2(P->wrows[0], P->wrows[1]), P->QT.p, P->WQT.p);
     MG_LAUNCHED();
-    MG_CUDA(cudaDeviceSynchronize());
+    // A device-resident q̃ belongs to the caller, who may release it once this returns; a
+    // host q̃ was staged into the plan's own buffer (freed stream-ordered), so the transposes
+    // may still run while the caller prepares the rows of its first execute.
+    if (qt_dev) MG_CUDA(cudaDeviceSynchronize());
 }
 
 
@@ -648,8 +651,13 @@ static inline bool lex_ge(int a2, int a3, int b2, int b3) {
 
 void build_rows(const mg_plan* P, int l2a, int l2b, const int* s, const int* e,
                 std::vector<MgRow>& rows) {
+    build_rows_range(P->l_min, P->l_max, l2a, l2b, s, e, rows);
+}
+
+void build_rows_range(int lmin, int lmax, int l2a, int l2b, const int* s, const int* e,
+                      std::vector<MgRow>& rows) {
     rows.clear();
-    const int lmin = P->l_min, lmax = P->l_max;
+    const int l0[2] = {(lmin & 1) ? lmin + 1 : lmin, (lmin & 1) ? lmin : lmin + 1};
     l2a = std::max(l2a, lmin);
     l2b = std::min(l2b, lmax + 1);
     for (int l2 = l2a; l2 < l2b; ++l2) {
@@ -669,8 +677,8 @@ void build_rows(const mg_plan* P, int l2a, int l2b, const int* s, const int* e,
                 if (lo > hi) continue;
                 MgRow r;
                 r.l2 = l2; r.l3 = l3; r.par = par;
-                r.jlo = (lo - P->l0[par]) / 2;
-                r.jhi = (hi - P->l0[par]) / 2;
+                r.jlo = (lo - l0[par]) / 2;
+                r.jhi = (hi - l0[par]) / 2;
                 r.pad = 0;
                 rows.push_back(r);
             }
@@ -1088,8 +1096,8 @@ static void set_rows(mg_plan* P, std::vector<MgRow>&& rows) {
         pre.hzoff[i + 1] = pre.hzoff[i] + (pre.hrows[i].jhi - pre.hrows[i].jlo + 1);
 }
 
-void execute_rows(mg_plan* P, const std::vector<MgRow>& rows, cudaStream_t st) {
-    set_rows(P, std::vector<MgRow>(rows));
+void execute_rows(mg_plan* P, std::vector<MgRow>&& rows, cudaStream_t st) {
+    set_rows(P, std::move(rows));
     if (P->prep.hrows.empty()) return zero_result(P, st);
     run_pipeline(P, P->prep.hrows, P->prep.hzoff, st, nullptr, nullptr, nullptr, nullptr,
                  nullptr, nullptr);
@@ -1159,7 +1167,7 @@ void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int
         i = j;
     }
     if (rows.empty()) {
-        execute_rows(P, rows, st);
+        execute_rows(P, std::move(rows), st);
         return;
     }
     P->prep.valid = false;

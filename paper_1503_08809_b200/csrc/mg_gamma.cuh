@@ -111,7 +111,10 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
 // Rows of the l2-slab [l2a, l2b) clipped to the flat range (s1,s2,s3) <= t < (e1,e2,e3).
 void build_rows(const mg_plan* P, int l2a, int l2b, const int* s, const int* e,
                 std::vector<MgRow>& rows);
-void execute_rows(mg_plan* P, const std::vector<MgRow>& rows, cudaStream_t st);
+// Same without a plan (host only; safe to run on another thread while the plan is built).
+void build_rows_range(int l_min, int l_max, int l2a, int l2b, const int* s, const int* e,
+                      std::vector<MgRow>& rows);
+void execute_rows(mg_plan* P, std::vector<MgRow>&& rows, cudaStream_t st);
 void execute_slab(mg_plan* P, int l2a, int l2b, cudaStream_t st);
 void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
                      int64_t count, cudaStream_t st);

@@ -1,8 +1,3 @@
 mkdir -p gpurun_out
-for v in prev t64bk32 t64bk16 prev t64bk32 t64bk16; do
-  export MG_LIB_PATH=$PWD/paper_1503_08809_b200/_native/variants/$v.so
-  for sl in "300 420" "1500 1540"; do
-    echo "== $v slab $sl"; timeout 200 python tools/time_slab.py --config c1 --l2 $sl --reps 3 2>&1 | tail -1
-  done
-done > gpurun_out/var.log 2>&1
-cat gpurun_out/var.log
+timeout 900 python -m pytest tests/test_gpu_gamma.py -m gpu -q -x > gpurun_out/pytest_gamma.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gamma.log
+timeout 300 python tools/e2e_breakdown.py 2>&1 | tail -3
