@@ -130,7 +130,7 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
              const double* __restrict__ q, int L, int l_min, int p,
              const double* __restrict__ C, const double* __restrict__ v,
              const double* __restrict__ lf, const double* __restrict__ fl, int mode,
-             double* __restrict__ panel) {
+             double* __restrict__ panel, unsigned magic_p) {
     extern __shared__ double zs[];  // [nrows][PANEL_JC]: zm of (row, j) for this chunk
     const MgTile tl = tiles[blockIdx.x];
     const int kt = (tl.jhi - tl.jlo + RUN_BK) / RUN_BK * RUN_BK;
@@ -163,7 +163,8 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
             if (jc + jl >= kt) break;
             double val = 0.0;
             if (slot < tl.nslots) {
-                const int rr = (tl.c0 + slot) / p, c = (tl.c0 + slot) % p;
+                const int cm = tl.c0 + slot, rr = (int)(((unsigned)cm * magic_p) >> 16),
+                          c = cm - rr * p;  // (c0 + slot) / p, % p (exact: cm < p + 128)
                 const double z = zs[rr * PANEL_JC + jl];
                 if (z != 0.0) {
                     const int l1 = l0[par] + 2 * (tl.jlo + jc + jl);
@@ -228,7 +229,8 @@ __global__ void __launch_bounds__(RunPipeP::THREADS, 1)
 k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __restrict__ poff,
                const double* __restrict__ panel, int row_base, const MgRow* __restrict__ rows,
                const double* __restrict__ WQB, int p, int Nx, int Nxw, int NxP,
-               longlong2 wbase, int2 wrows, double* __restrict__ H) {
+               longlong2 wbase, int2 wrows, double* __restrict__ H, unsigned magic_p,
+               unsigned magic_nx) {
     extern __shared__ __align__(16) double smem[];
     const int64_t ldb = (int64_t)p * Nxw;
     RunItems items{tiles, poff, panel, rows, WQB, wbase, wrows, (int)((ldb + RUN_TN - 1) / RUN_TN)};
@@ -239,8 +241,7 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
         const int ti = it / items.NB, nb = it - ti * items.NB;
         const MgTile tl = tiles[ti];
         const int n0 = nb * RUN_TN;
-        const int hbase = (tl.row0 - row_base) * p + tl.c0;  // H row of slot 0
-        // Per-thread offsets, computed once per item (no divisions in the store loop):
+        // Per-thread offsets, computed once per item (no divisions at all):
         // slot (rr, c) -> (rr*XB*pp + c*p)*X_LDK ; column gn = c'*Nxw + x ->
         // ((x/32)*pp + c')*X_LDK + x%32   (Nxw even: columns gn, gn+1 share c' and x-block)
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -251,14 +252,16 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
 #pragma unroll
         for (int fm = 0; fm < CfgRun::FM; ++fm) {
             const int m = wm + fm * 8;
-            const int slot = (int)hbase + m, rr = slot / p;  // < nb1 * p: 32-bit division
+            // (c0 + m) / p by multiply-shift (c0 + m < p + 128: exact with a 16-bit magic)
+            const int cm = tl.c0 + m, dq = (int)(((unsigned)cm * magic_p) >> 16);
+            const int rr = tl.row0 - row_base + dq, c = cm - dq * p;
             rok[fm] = m < tl.nslots;
-            roff[fm] = ((int64_t)rr * XB * pp + (int64_t)(slot - rr * p) * p) * X_LDK;
+            roff[fm] = ((int64_t)rr * XB * pp + (int64_t)c * p) * X_LDK;
         }
 #pragma unroll
         for (int fn = 0; fn < CfgRun::FN; ++fn) {
             const int gn = n0 + wn + fn * 8;
-            const int cp = gn / Nxw, x = gn - cp * Nxw;
+            const int cp = (int)__umulhi((unsigned)gn, magic_nx), x = gn - cp * Nxw;  // gn / Nxw
             const bool both = gn < ldb && x + 1 < Nx, one = gn < ldb && x < Nx;
             const int64_t coff = ((int64_t)(x / X_BK) * pp + cp) * X_LDK + (x & (X_BK - 1));
 #pragma unroll
@@ -963,7 +966,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                        os>>>(
             P->prep.tiles_d.p + tf, P->prep.rows.p, P->prep.poff.p + tf, P->prep.zoff.p, zbase,
             zt, P->l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p, P->fl.p,
-            P->h2_mode, panel_buf[k & 1]);
+            P->h2_mode, panel_buf[k & 1], (65536u + p - 1) / p);
         MG_LAUNCHED();
     };
 
@@ -1017,7 +1020,8 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             P->prep.tiles_d.p + tf, tl - tf, P->prep.poff.p + tf, panel_buf[k & 1], (int)B.b1,
             P->prep.rows.p, P->WQT.p, p, P->Nx, P->Nxw, NxP,
             make_longlong2(P->wbase[0], P->wbase[1]), make_int2(P->wrows[0], P->wrows[1]),
-            P->sc->H.p);
+            P->sc->H.p, (65536u + p - 1) / p,
+            (unsigned)(((1ull << 32) + P->Nxw - 1) / P->Nxw));
         MG_LAUNCHED();
 #if MG_SIDE
         prof_mark(P, 0, ms);

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_gamma.py -m gpu -q -x > gpurun_out/pytest_gamma.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gamma.log
-timeout 300 python tools/e2e_breakdown.py 2>&1 | tail -3
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['e2e'], d['roofline']['kernel_ms_per_step'])"
