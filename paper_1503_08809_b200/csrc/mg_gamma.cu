@@ -302,7 +302,19 @@ constexpr int PP_CHUNK = 16;  // pairs per block of the pair-product kernel
 // K2a: S[r][ab][x] = q̃_a(x,l2)q̃_b(x,l3) + q̃_b(x,l2)q̃_a(x,l3) in the x-blocked layout of the
 // x contraction.  One block per (row, chunk of 16 pairs); a thread owns an x pair (double2) and
 // walks the chunk b-major: q̃_b(l2), q̃_b(l3) stay in registers while four a's are loaded at once.
-__global__ void __launch_bounds__(256)
+#ifndef MG_PP_THREADS
+#define MG_PP_THREADS 128
+#endif
+#ifndef MG_PP_MAXREG
+#define MG_PP_MAXREG 32
+#endif
+#ifndef MG_PP_UNROLL
+#define MG_PP_UNROLL 2
+#endif
+// 128 threads x <= 32 registers: one warp per SM sub-partition, 1024 registers each, which
+// still fits beside a run-contraction CTA (17 warps x 96 registers leave one sub-partition
+// exactly 1024 free), so the side-stream pair products really run concurrently with it.
+__global__ void __maxnreg__(MG_PP_MAXREG)
 k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __restrict__ QT,
                 int p, int P2, int NxP, int l_min, double* __restrict__ S) {
     const int r = blockIdx.y;
@@ -322,15 +334,15 @@ k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __rest
             const double2 ub = __ldg(q2 + b * nx2 + x), wb = __ldg(q3 + b * nx2 + x);
             const int na = min(b + 1 - a, pr1 - pr);  // pairs (a .. a+na-1, b)
             int i = 0;
-            for (; i + 4 <= na; i += 4) {
-                double2 u[4], w[4];
+            for (; i + MG_PP_UNROLL <= na; i += MG_PP_UNROLL) {
+                double2 u[MG_PP_UNROLL], w[MG_PP_UNROLL];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < MG_PP_UNROLL; ++k) {
                     u[k] = __ldg(q2 + (a + i + k) * nx2 + x);
                     w[k] = __ldg(q3 + (a + i + k) * nx2 + x);
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < MG_PP_UNROLL; ++k)
                     *reinterpret_cast<double2*>(o + (int64_t)(pr + i + k) * X_LDK) =
                         make_double2(u[k].x * wb.x + ub.x * w[k].x, u[k].y * wb.y + ub.y * w[k].y);
             }
@@ -973,7 +985,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     auto issue_pairs = [&](int k, cudaStream_t os) {
         const Batch& B = batches[k];
         dim3 gs(ceil_div(P2, PP_CHUNK), (int)(B.e1 - B.b1));
-        k_pair_products<<<gs, 256, 0, os>>>(P->prep.rows.p, (int)B.b1, P->QT.p, p, P2, NxP,
+        k_pair_products<<<gs, MG_PP_THREADS, 0, os>>>(P->prep.rows.p, (int)B.b1, P->QT.p, p, P2, NxP,
                                              P->l_min, P->sc->S.p);
         MG_LAUNCHED();
     };
