@@ -16,13 +16,21 @@
 
 #include "mg_bessel.cuh"
 #include "mg_common.cuh"
+#include "mg_dmma.cuh"
 
 namespace mg {
 
 constexpr int QB_XT = 4;     // x values per CTA
 constexpr int QB_KT = 256;   // k per tile (= threads)
 constexpr int QB_LT = 8;     // l per chunk
-constexpr int QB_LDU = QB_KT + 1;
+#ifndef MG_QB_DMMA
+#define MG_QB_DMMA 1  // contraction over k on DMMA (1) or as per-thread DFMA dot products (0)
+#endif
+// row strides of the shared-memory u and b tiles: +4 keeps the m8n8k4 fragment reads (lane
+// (g,t) reads row 8f+g, column 4s+t) bank-conflict free; +1 the scalar dot products'
+constexpr int QB_LDU = MG_QB_DMMA ? QB_KT + 4 : QB_KT + 1;
+constexpr int QB_LDB = MG_QB_DMMA ? QB_KT + 4 : QB_KT;
+constexpr int QB_NC = QB_LT * QB_XT;  // (l, x) output columns per chunk = 32 = 4 n-fragments
 
 // Δ[l-l_min][k] for one thread per k (z = X k), plus b[c][k] = wk k^2 qk[c][k].
 __global__ void k_delta(const double* __restrict__ k, const double* __restrict__ wk, int Nk,
@@ -119,76 +127,142 @@ __global__ void k_qb_prepare(const double* __restrict__ k, int Nk, const double*
 }
 
 // One sweep (dir = +1 ascending/upward, -1 descending/Miller) over all l for XT x-values.
+// DMMA contraction (MG_QB_DMMA): per chunk, C[c][(l,x)] = Σ_k b[c][k] u[(l,x)][k] with
+// M = p (MF m-fragments), N = 32 (l,x) columns, K = Nk; warp w owns the k-slice
+// [32w, 32w+32) of every k-tile and all MF x 4 output fragments; the 8 warp partials are
+// summed in warp order at the end of the chunk (deterministic).
+template <int MF>
 __global__ void __launch_bounds__(QB_KT)
 k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restrict__ x, int Nx,
            const double* __restrict__ delta, const double* __restrict__ b, int p, int l_min,
            int l_max, QState st, double* __restrict__ qt) {
     extern __shared__ double sh[];
     double* us = sh;                                   // [LT][XT][LDU]
-    double* bs = sh + QB_LT * QB_XT * QB_LDU;          // [p][KT]
+    double* bs = sh + QB_LT * QB_XT * QB_LDU;          // [MF*8][LDB] (rows >= p stay zero)
     const int x0 = blockIdx.x * QB_XT;
+#if MG_QB_DMMA
+    for (int i = threadIdx.x; i < (MF * 8 - p) * QB_LDB; i += QB_KT) bs[p * QB_LDB + i] = 0.0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+#endif
     const int L = l_max - l_min + 1;
+#if !MG_QB_DMMA
     const int nout = p * QB_XT * QB_LT;
+#endif
     const int nchunk = (L + QB_LT - 1) / QB_LT;
     for (int ch = 0; ch < nchunk; ++ch) {
         // chunk covers l = lc0 + dir*li, li < nl
         const int lc0 = dir > 0 ? l_min + ch * QB_LT : l_max - ch * QB_LT;
         const int nl = min(QB_LT, L - ch * QB_LT);
+#if MG_QB_DMMA
+        double cf[MF][4][2];
+#pragma unroll
+        for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf) cf[mf][nf][0] = cf[mf][nf][1] = 0.0;
+#else
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#endif
         for (int kt = 0; kt < Nk; kt += QB_KT) {
             const int ki = kt + threadIdx.x;
             bool any = false;
+            // the XT recurrences of this k advance together (l outer, x inner): XT independent
+            // dependency chains per step instead of one long chain per x
+            bool okp[QB_XT], live_u[QB_XT];
+            double z[QB_XT];
+            int lsw[QB_XT];
+            int64_t si[QB_XT];
+#pragma unroll
             for (int xi = 0; xi < QB_XT; ++xi) {
                 const int xg = x0 + xi;
-                const bool okp = ki < Nk && xg < Nx;
-                const int64_t si = (int64_t)xg * Nk + ki;
-                double z = okp ? k[ki] * x[xg] : 1.0;
-                int lsw = okp ? st.lsw[si] : l_max;
-                const bool live_u = okp && z > 0.0;  // z = 0 contributes nothing
-                if (dir > 0) {
-                    double jm = okp ? st.ua[si] : 0.0, jc = okp ? st.ub[si] : 0.0;
-                    for (int li = 0; li < QB_LT; ++li) {
-                        int l = lc0 + li;
+                okp[xi] = ki < Nk && xg < Nx;
+                si[xi] = (int64_t)xg * Nk + ki;
+                z[xi] = okp[xi] ? k[ki] * x[xg] : 1.0;
+                lsw[xi] = okp[xi] ? st.lsw[si[xi]] : l_max;
+                live_u[xi] = okp[xi] && z[xi] > 0.0;  // z = 0 contributes nothing
+            }
+            if (dir > 0) {
+                double jm[QB_XT], jc[QB_XT];
+#pragma unroll
+                for (int xi = 0; xi < QB_XT; ++xi) {
+                    jm[xi] = okp[xi] ? st.ua[si[xi]] : 0.0;
+                    jc[xi] = okp[xi] ? st.ub[si[xi]] : 0.0;
+                }
+                for (int li = 0; li < QB_LT; ++li) {
+                    const int l = lc0 + li;
+                    const double dl = li < nl ? delta[(int64_t)(l - l_min) * Nk + min(ki, Nk - 1)] : 0.0;
+#pragma unroll
+                    for (int xi = 0; xi < QB_XT; ++xi) {
                         double u = 0.0;
-                        if (live_u && li < nl && l <= lsw) {
-                            double jn = bessel_step(l - 1, jc, jm, z);
-                            jm = jc;
-                            jc = jn;
-                            u = delta[(int64_t)(l - l_min) * Nk + ki] * jn;
+                        if (live_u[xi] && li < nl && l <= lsw[xi]) {
+                            const double jn = bessel_step(l - 1, jc[xi], jm[xi], z[xi]);
+                            jm[xi] = jc[xi];
+                            jc[xi] = jn;
+                            u = dl * jn;
                             any = true;
                         }
                         us[(li * QB_XT + xi) * QB_LDU + threadIdx.x] = u;
                     }
-                    if (okp) { st.ua[si] = jm; st.ub[si] = jc; }
-                } else {
-                    double jp = okp ? st.da[si] : 0.0, jd = okp ? st.db[si] : 0.0;
-                    int s = okp ? st.ds[si] : 0;
-                    BesselNorm bn;
-                    bn.norm = okp ? st.nrm[si] : 0.0;
-                    bn.stot = okp ? st.stot[si] : 0;
-                    for (int li = 0; li < QB_LT; ++li) {
-                        int l = lc0 - li;
+                }
+#pragma unroll
+                for (int xi = 0; xi < QB_XT; ++xi)
+                    if (okp[xi]) { st.ua[si[xi]] = jm[xi]; st.ub[si[xi]] = jc[xi]; }
+            } else {
+                double jp[QB_XT], jd[QB_XT];
+                int sc[QB_XT];
+                BesselNorm bn[QB_XT];
+#pragma unroll
+                for (int xi = 0; xi < QB_XT; ++xi) {
+                    jp[xi] = okp[xi] ? st.da[si[xi]] : 0.0;
+                    jd[xi] = okp[xi] ? st.db[si[xi]] : 0.0;
+                    sc[xi] = okp[xi] ? st.ds[si[xi]] : 0;
+                    bn[xi].norm = okp[xi] ? st.nrm[si[xi]] : 0.0;
+                    bn[xi].stot = okp[xi] ? st.stot[si[xi]] : 0;
+                }
+                for (int li = 0; li < QB_LT; ++li) {
+                    const int l = lc0 - li;
+                    const double dl = li < nl ? delta[(int64_t)(l - l_min) * Nk + min(ki, Nk - 1)] : 0.0;
+#pragma unroll
+                    for (int xi = 0; xi < QB_XT; ++xi) {
                         double u = 0.0;
-                        if (live_u && li < nl && l > lsw) {
-                            u = delta[(int64_t)(l - l_min) * Nk + ki] * bessel_denorm(jd, s, bn);
+                        if (live_u[xi] && li < nl && l > lsw[xi]) {
+                            u = dl * bessel_denorm(jd[xi], sc[xi], bn[xi]);
                             any = true;
-                            double jn = bessel_step(l, jd, jp, z);  // jhat_{l-1}
-                            jp = jd;
-                            jd = jn;
-                            if (fabs(jd) > MGB_BIG) {
-                                jd = ldexp(jd, -MGB_SHIFT);
-                                jp = ldexp(jp, -MGB_SHIFT);
-                                ++s;
+                            const double jn = bessel_step(l, jd[xi], jp[xi], z[xi]);  // jhat_{l-1}
+                            jp[xi] = jd[xi];
+                            jd[xi] = jn;
+                            if (fabs(jd[xi]) > MGB_BIG) {
+                                jd[xi] = ldexp(jd[xi], -MGB_SHIFT);
+                                jp[xi] = ldexp(jp[xi], -MGB_SHIFT);
+                                ++sc[xi];
                             }
                         }
                         us[(li * QB_XT + xi) * QB_LDU + threadIdx.x] = u;
                     }
-                    if (okp) { st.da[si] = jp; st.db[si] = jd; st.ds[si] = s; }
                 }
+#pragma unroll
+                for (int xi = 0; xi < QB_XT; ++xi)
+                    if (okp[xi]) { st.da[si[xi]] = jp[xi]; st.db[si[xi]] = jd[xi]; st.ds[si[xi]] = sc[xi]; }
             }
             for (int c = 0; c < p; ++c)
-                bs[c * QB_KT + threadIdx.x] = ki < Nk ? b[(int64_t)c * Nk + ki] : 0.0;
+                bs[c * QB_LDB + threadIdx.x] = ki < Nk ? b[(int64_t)c * Nk + ki] : 0.0;
             const int live = __syncthreads_or(any);
+#if MG_QB_DMMA
+            if (live) {  // u, b past Nk are zero, so the full k-slice is summed
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const int kk = warp * 32 + ks * 4 + t4;
+                    double af[MF], bf[4];
+#pragma unroll
+                    for (int mf = 0; mf < MF; ++mf) af[mf] = bs[(mf * 8 + g) * QB_LDB + kk];
+#pragma unroll
+                    for (int nf = 0; nf < 4; ++nf) bf[nf] = us[(nf * 8 + g) * QB_LDU + kk];
+#pragma unroll
+                    for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+                        for (int nf = 0; nf < 4; ++nf) dmma884(cf[mf][nf], af[mf], bf[nf]);
+                }
+            }
+#else
             if (live) {
                 const int kn = min(QB_KT, Nk - kt);
                 for (int r = 0; r < 4; ++r) {
@@ -203,8 +277,33 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
                     }
                 }
             }
+#endif
             __syncthreads();
         }
+#if MG_QB_DMMA
+        // warp partials -> us (free after the last k-tile), then summed in warp order
+        double* red = us;  // [8 warps][MF*8][32]
+#pragma unroll
+        for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf) {
+                const int m = mf * 8 + g, n = nf * 8 + 2 * t4;
+                red[(warp * MF * 8 + m) * QB_NC + n] = cf[mf][nf][0];
+                red[(warp * MF * 8 + m) * QB_NC + n + 1] = cf[mf][nf][1];
+            }
+        __syncthreads();
+        for (int o = threadIdx.x; o < p * QB_NC; o += QB_KT) {
+            const int c = o / QB_NC, n = o % QB_NC, li = n / QB_XT, xi = n % QB_XT;
+            double v = 0.0;
+            for (int w = 0; w < QB_KT / 32; ++w) v += red[(w * MF * 8 + c) * QB_NC + n];
+            const int l = lc0 + dir * li, xg = x0 + xi;
+            if (li < nl && xg < Nx) {
+                const int64_t oi = ((int64_t)c * Nx + xg) * L + (l - l_min);
+                qt[oi] = dir > 0 ? v : qt[oi] + v;
+            }
+        }
+        __syncthreads();  // red aliases us
+#else
         for (int r = 0; r < 4; ++r) {
             int o = threadIdx.x + r * QB_KT;
             if (o < nout) {
@@ -216,7 +315,18 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
                 }
             }
         }
+#endif
     }
+}
+
+template <int MF>
+static void launch_qb_sweep(int grid, size_t shm, cudaStream_t s, int dir, const double* k, int Nk,
+                            const double* x, int Nx, const double* delta, const double* b, int p,
+                            int l_min, int l_max, QState st, double* qt) {
+    MG_CUDA(cudaFuncSetAttribute(k_qb_sweep<MF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)shm));
+    k_qb_sweep<MF><<<grid, QB_KT, shm, s>>>(dir, k, Nk, x, Nx, delta, b, p, l_min, l_max, st, qt);
+    MG_LAUNCHED();
 }
 
 // Build Δ, C and q̃ on the device.  Inputs are host arrays; outputs device buffers
@@ -257,16 +367,18 @@ void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x
         k_qb_prepare<<<(int)std::min<size_t>((np + 255) / 256, 148 * 64), 256, 0, s>>>(
             dk.p, Nk, dx.p, Nx, l_min, l_max, st);
         MG_LAUNCHED();
-        const size_t shm = (size_t)(QB_LT * QB_XT * QB_LDU + p * QB_KT) * sizeof(double);
-        MG_CUDA(cudaFuncSetAttribute(k_qb_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)shm));
+        const int mf = (p + 7) / 8;
+        const size_t shm =
+            (size_t)(QB_LT * QB_XT * QB_LDU + (MG_QB_DMMA ? mf * 8 : p) * QB_LDB) * sizeof(double);
         const int grid = (Nx + QB_XT - 1) / QB_XT;
-        k_qb_sweep<<<grid, QB_KT, shm, s>>>(+1, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max,
-                                            st, qt_dev);
-        MG_LAUNCHED();
-        k_qb_sweep<<<grid, QB_KT, shm, s>>>(-1, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max,
-                                            st, qt_dev);
-        MG_LAUNCHED();
+        for (int dir : {+1, -1}) {
+            switch (MG_QB_DMMA ? mf : 1) {
+                case 1: launch_qb_sweep<1>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max, st, qt_dev); break;
+                case 2: launch_qb_sweep<2>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max, st, qt_dev); break;
+                case 3: launch_qb_sweep<3>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max, st, qt_dev); break;
+                default: launch_qb_sweep<4>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max, st, qt_dev); break;
+            }
+        }
         MG_CUDA(cudaStreamSynchronize(s));  // temporaries die with this scope
     } else {
         MG_CUDA(cudaStreamSynchronize(s));
