@@ -20,9 +20,12 @@
 
 namespace mg {
 
-constexpr int QB_XT = 4;     // x values per CTA
-constexpr int QB_KT = 256;   // k per tile (= threads)
-constexpr int QB_LT = 8;     // l per chunk
+#ifndef MG_QB_XT
+#define MG_QB_XT 2  // measured: 2 beats 4 at c1 (0.042 vs 0.056 s), ties at c4; 1 is slower
+#endif
+constexpr int QB_XT = MG_QB_XT;       // x values per CTA
+constexpr int QB_KT = 256;            // k per tile (= threads)
+constexpr int QB_LT = 32 / QB_XT;     // l per chunk (XT * LT = 32 output columns)
 #ifndef MG_QB_DMMA
 #define MG_QB_DMMA 1  // contraction over k on DMMA (1) or as per-thread DFMA dot products (0)
 #endif

@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-tail -1 gpurun_out/pytest_s1.log 2>/dev/null
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_qb_sweep -c 2 -o gpurun_out/prof_qb python tools/time_qtilde.py c4 1 > gpurun_out/ncu_qb.log 2>&1; echo "ncu rc=$?"
+for v in default qxt1 qxt2; do
+  if [ $v = default ]; then unset MG_LIB_PATH; else export MG_LIB_PATH=$PWD/paper_1503_08809_b200/_native/variants/$v.so; fi
+  echo "== $v"; timeout 300 python tools/time_qtilde.py c1 3 2>&1 | tail -1; timeout 300 python tools/time_qtilde.py c4 2 2>&1 | tail -1
+done
