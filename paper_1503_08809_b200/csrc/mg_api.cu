@@ -208,9 +208,15 @@ int mg_plan_stats(mg_plan* P, double* f_run, double* f_x, double* f_pair, int64_
 int mg_plan_set_profile(mg_plan* P, int on) {
     return guarded([&] {
         MG_REQUIRE(P, "null plan");
+        DeviceGuard g(P->device);
+        if (P->prof_used) MG_CUDA(cudaEventSynchronize(P->prof_events[P->prof_used - 1]));
+        if (P->side_used) MG_CUDA(cudaEventSynchronize(P->side_events[P->side_used - 1]));
         P->profile = on != 0;
         for (double& m : P->prof_ms) m = 0.0;
         P->ns_used = 0;
+        P->prof_used = 0;
+        P->side_used = 0;
+        P->prof_tags.clear();
     });
 }
 
@@ -218,6 +224,7 @@ int mg_plan_kernel_ms(mg_plan* P, double* ms) {
     return guarded([&] {
         MG_REQUIRE(P && ms, "null argument");
         DeviceGuard g(P->device);
+        prof_collect(P);
         nonsep_collect(P);
         for (int i = 0; i < MG_NPROF; ++i) ms[i] = P->prof_ms[i];
     });

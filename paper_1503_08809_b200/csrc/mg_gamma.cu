@@ -31,16 +31,11 @@
 
 namespace mg {
 
-#ifndef MG_RUN_TILE96
-#define MG_RUN_TILE96 1
+#ifndef MG_RUN_WARPS
+#define MG_RUN_WARPS 12  // consumer warps of the 128 x 96 run/pair tile: 12 (32x32 per warp) or 16
 #endif
-#if MG_RUN_TILE96
 constexpr int RUN_TN = 96;              // run-contraction N tile ((c', x) columns)
 constexpr int RUN_TM_ = 128;            // (row, c) slots per tile
-#else
-constexpr int RUN_TN = 120;
-constexpr int RUN_TM_ = 120;
-#endif
 constexpr int RUN_LDB = RUN_TN + 4;     // smem-identical row stride of WQB rows
 constexpr int RUN_LDA = RUN_TM_ + 4;    // smem-identical row stride of the A panels
 
@@ -108,12 +103,15 @@ constexpr int RUN_BK = MG_RUN_BK, RUN_ST = MG_RUN_ST;
 constexpr int X_BK = 32;
 constexpr int X_LDK = X_BK + 4;  // x-blocked S/H row stride: [row][x/32][m][36], smem-identical
 using CfgX120 = TileCfg<5, 3, 3, 5>;  // 120 x 120, 15 warps, 30 accumulators per lane
-// run contraction: 16 consumer warps (4 per SM sub-partition, so every DMMA unit has the same
-// number of warps to serve) + 1 producer warp; 128 packed (row,c) slots x 96 columns
-#if MG_RUN_TILE96
-using CfgRun = TileCfg<4, 4, 4, 3>;
+// run contraction: 128 packed (row,c) slots x 96 columns; the consumer warps are a multiple
+// of 4 so every SM sub-partition's DMMA unit serves the same number of warps
+#if MG_RUN_WARPS == 12
+// 12 consumer warps (3 per SM sub-partition, 4x4 fragments each) + 1 producer: 13 warps
+// allocate 128 registers per thread, so the accumulators and double-buffered fragments fit
+// without spills (16 consumer warps + producer cap at 96 and spill)
+using CfgRun = TileCfg<4, 3, 4, 4>;
 #else
-using CfgRun = CfgX120;
+using CfgRun = TileCfg<4, 4, 4, 3>;
 #endif
 constexpr int RUN_TM = CfgRun::BM;     // (row, c) slots per run tile = A panel width
 static_assert(RUN_TN == CfgRun::BN && RUN_TM == RUN_TM_ && RUN_LDA == ld_kmajor(RUN_TM) &&
@@ -620,6 +618,7 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
     P->hv.assign(v, v + L);
 
     P->q.upload(q, (size_t)p * L);
+    P->l0d.upload(P->l0, 2);
     {
         std::vector<double> fl(L);
         for (int i = 0; i < L; ++i)
@@ -764,8 +763,9 @@ static void plan_streams(mg_plan* P) {
         MG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
-static void prof_collect(mg_plan* P) {
-    if (!P->profile) return;
+void prof_collect(mg_plan* P) {
+    if (P->side_used) MG_CUDA(cudaEventSynchronize(P->side_events[P->side_used - 1]));
+    if (P->prof_used) MG_CUDA(cudaEventSynchronize(P->prof_events[P->prof_used - 1]));
     for (size_t i = 0; i + 1 < P->side_used; i += 2) {
         float ms = 0.f;
         MG_CUDA(cudaEventElapsedTime(&ms, P->side_events[i], P->side_events[i + 1]));
@@ -938,8 +938,6 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         for (int k = 0; k < 2; ++k) MG_CUDA(cudaStreamWaitEvent(x, P->ev_start[k], 0));
     if (zero_h) MG_CUDA(cudaMemsetAsync(P->sc->H.p, 0, P->sc->H.n * sizeof(double), ms));
     MG_CUDA(cudaMemsetAsync(P->sc->Z.p, 0, (size_t)nsplit * zsplit * sizeof(double), ms));
-    P->l0d.upload(P->l0, 2, ms);
-    MG_CUDA(cudaStreamSynchronize(ms));  // l0 comes from pageable host memory
     prof_mark(P, 0, ms);
 
     struct Batch { int64_t b1, e1, b3, e3; int bidx; };
@@ -1088,11 +1086,10 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     // the caller's stream (and stream 0, which frees/reallocates scratch) resume after both
     MG_CUDA(cudaEventRecord(P->ev_end[0], ms));
     MG_CUDA(cudaEventRecord(P->ev_end[1], ss));
+    // No host synchronisation: the execute is asynchronous (include/modal_b200.h); kernel
+    // timings are resolved when they are read (prof_collect).
     for (cudaStream_t x : {st, (cudaStream_t)0})
         for (int k = 0; k < 2; ++k) MG_CUDA(cudaStreamWaitEvent(x, P->ev_end[k], 0));
-    MG_CUDA(cudaStreamSynchronize(ms));
-    MG_CUDA(cudaStreamSynchronize(ss));
-    prof_collect(P);
 }
 
 static void zero_result(mg_plan* P, cudaStream_t st) {

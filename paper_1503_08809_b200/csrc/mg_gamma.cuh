@@ -123,6 +123,8 @@ void nonsep_set_domain(mg_plan* P, const int32_t* l1, const int32_t* l2, const i
 void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_host,
                     cudaStream_t st);
 void nonsep_collect(mg_plan* P);
+// Resolve the recorded per-launch timing events of profiled executes into prof_ms.
+void prof_collect(mg_plan* P);
 void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l2,
             const int32_t* l3, const double* W, int64_t count, double* b, cudaStream_t st);
 void weights(int l_min, int l_max, const double* C, const double* v, int h2_mode,
