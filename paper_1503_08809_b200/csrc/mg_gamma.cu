@@ -421,7 +421,14 @@ k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int n
     }, smem);
 }
 
-using CfgX160 = TileCfg<4, 4, 5, 3>;   // 160 x 96, 16 consumer warps (p = 30)
+#ifndef MG_X160_WARPS
+#define MG_X160_WARPS 12
+#endif
+#if MG_X160_WARPS == 12
+using CfgX160 = TileCfg<4, 3, 5, 4>;   // 160 x 96, 12 consumer warps, 128 registers (p = 30)
+#else
+using CfgX160 = TileCfg<4, 4, 5, 3>;   // 160 x 96, 16 consumer warps (96 registers, spills)
+#endif
 using CfgX128 = TileCfg<2, 4, 8, 4>;   // 128 x 128, 8 consumer warps (p = 22)
 
 // Tile choice for the x contraction: padded-area efficiency of M = p(p+1)/2, N = p^2, times
