@@ -221,6 +221,31 @@ class TestGammaLarge:
         plan.execute()
         assert np.array_equal(plan.fetch(), full)              # bitwise reproducible
 
+    def test_async_executes_into_device_buffers(self, c1):
+        """mg_plan_execute is asynchronous: back-to-back executes into device tensors on a
+        side stream, no host sync in between, match the synchronous per-slab results."""
+        import torch
+        hi, C, qt = c1
+        plan = GammaPlan(hi.q, qt, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max)
+        n = hi.entries.shape[0]
+        bounds = [(2, 400), (400, 800), (800, 1000)]
+        want = []
+        for a, b in bounds:
+            plan.execute(a, b)
+            want.append(plan.fetch())
+        s = torch.cuda.Stream()
+        outs = [torch.empty((n, n), dtype=torch.float64, device="cuda") for _ in bounds]
+        with torch.cuda.stream(s):
+            for (a, b), o in zip(bounds, outs):
+                plan.execute(a, b, out=o, stream=s)
+        s.synchronize()
+        for o, w in zip(outs, want):
+            assert np.array_equal(o.cpu().numpy(), w)
+        plan.set_profile(True)
+        plan.execute(2, 400, stream=s)
+        ms = plan.kernel_ms()                                  # resolves the pending events
+        assert ms["run"] > 0 and ms["x"] > 0
+
 
 @pytest.mark.parametrize("cfg,ntri", [("c2", 1500), ("c4", 160)])
 def test_large_config_partials(cfg, ntri):
