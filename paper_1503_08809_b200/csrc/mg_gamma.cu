@@ -192,9 +192,14 @@ struct RunItems {
     longlong2 wbase;
     int2 wrows;
     int NB;
+    int ldb;  // p * Nxw columns
     __device__ int ktiles(int it) const {
         const MgTile& t = tiles[it / NB];
         return (t.jhi - t.jlo + RUN_BK) / RUN_BK;
+    }
+    __device__ int2 valid_mn(int it) const {
+        const int ti = it / NB;
+        return make_int2(tiles[ti].nslots, min(RUN_TN, ldb - (it - ti * NB) * RUN_TN));
     }
     __device__ int kvalid_last(int it) const {
         const MgTile& t = tiles[it / NB];
@@ -221,7 +226,7 @@ struct RunItems {
         }
     }
 };
-using RunPipeP = PipeTMAPersistent<CfgRun, RUN_BK, RUN_ST, true, true>;
+using RunPipeP = PipeTMAPersistent<CfgRun, RUN_BK, RUN_ST, true, true, true>;
 
 __global__ void __launch_bounds__(RunPipeP::THREADS, 1)
 k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __restrict__ poff,
@@ -231,7 +236,8 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
                unsigned magic_nx) {
     extern __shared__ __align__(16) double smem[];
     const int64_t ldb = (int64_t)p * Nxw;
-    RunItems items{tiles, poff, panel, rows, WQB, wbase, wrows, (int)((ldb + RUN_TN - 1) / RUN_TN)};
+    RunItems items{tiles, poff, panel, rows, WQB, wbase, wrows, (int)((ldb + RUN_TN - 1) / RUN_TN),
+                   (int)ldb};
     const int nitems = ntiles * items.NB;
     const int64_t pp = (int64_t)p * p;
     const int XB = NxP / X_BK;
@@ -370,6 +376,11 @@ struct XItems {
     }
     __device__ int ktiles(int) const { return XB; }
     __device__ int kvalid_last(int) const { return kv_last; }
+    __device__ int2 valid_mn(int it) const {
+        int r, mt, nt;
+        decode(it, r, mt, nt);
+        return make_int2(min(Cfg::BM, P2 - mt * Cfg::BM), min(Cfg::BN, pp - nt * Cfg::BN));
+    }
     __device__ uint32_t stage_bytes(int it, int) const {
         int r, mt, nt;
         decode(it, r, mt, nt);
@@ -508,7 +519,13 @@ struct PairItems {
         mt = (it / NT) % MT;
         s = it / (NT * MT);
     }
+    int P2, ncols;
     __device__ int rows_of(int s) const { return min(per, n3 - s * per); }
+    __device__ int2 valid_mn(int it) const {
+        int s, mt, nt;
+        decode(it, s, mt, nt);
+        return make_int2(min(RUN_TM, P2 - mt * RUN_TM), min(RUN_TN, ncols - nt * RUN_TN));
+    }
     __device__ int ktiles(int it) const {
         int s, mt, nt;
         decode(it, s, mt, nt);
@@ -544,7 +561,7 @@ k_pair_contract(const double* __restrict__ SqB, const double* __restrict__ RB, i
                 double* __restrict__ Z) {
     extern __shared__ __align__(16) double smem[];
     PairItems items{SqB, RB, kp, n3, per, (P2 + RUN_TM - 1) / RUN_TM,
-                    (ncols + RUN_TN - 1) / RUN_TN};
+                    (ncols + RUN_TN - 1) / RUN_TN, P2, ncols};
     const int nitems = nsplit * items.MT * items.NT;
     RunPipeP::run(blockIdx.x, gridDim.x, nitems, items, [&](int it, const Acc<CfgRun>& acc) {
         int s, mt, nt;
