@@ -432,14 +432,11 @@ k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int n
     }, smem);
 }
 
-#ifndef MG_X160_WARPS
-#define MG_X160_WARPS 12
-#endif
-#if MG_X160_WARPS == 12
-using CfgX160 = TileCfg<4, 3, 5, 4>;   // 160 x 96, 12 consumer warps, 128 registers (p = 30)
-#else
-using CfgX160 = TileCfg<4, 4, 5, 3>;   // 160 x 96, 16 consumer warps (96 registers, spills)
-#endif
+// second x-contraction tile (chosen for p = 30): 120 x 96 on 12 consumer warps (5x3
+// fragments each, 120 registers, no spills).  Measured at config 4: 1 % faster than 160 x 96
+// on 12 warps (5x4 fragments, spills 60 B) and 3 % faster than 160 x 96 on 16 warps
+// (96-register cap, spills); M = 465 pads to 480 in both.
+using CfgX160 = TileCfg<3, 4, 5, 3>;
 using CfgX128 = TileCfg<2, 4, 8, 4>;   // 128 x 128, 8 consumer warps (p = 22)
 
 // Tile choice for the x contraction: padded-area efficiency of M = p(p+1)/2, N = p^2, times
@@ -450,7 +447,7 @@ static XTile choose_xtile(int P2, int pp) {
     auto eff = [&](int bm, int bn, double bal) {
         return bal * (double)P2 * pp / ((double)ceil_div(P2, bm) * bm * ceil_div(pp, bn) * bn);
     };
-    const double e120 = eff(120, 120, 15.0 / 16.0), e160 = eff(160, 96, 1.0),
+    const double e120 = eff(120, 120, 15.0 / 16.0), e160 = eff(CfgX160::BM, CfgX160::BN, 1.0),
                  e128 = eff(128, 128, 1.0);
     if (e120 >= e160 && e120 >= e128) return XTile::T120;
     return e160 >= e128 ? XTile::T160 : XTile::T128;
