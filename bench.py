@@ -55,38 +55,49 @@ def parse():
 
 # ------------------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """nvidia-smi clocks / throttle reasons during the timed region.  One long-lived
+    `nvidia-smi -lms 200` process streams the samples (no fork per sample, so the sampler
+    cannot stall the launching thread)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_ms: int = 200):
         self.gpu = gpu
+        self.period_ms = period_ms
         self.samples = []
-        self._stop = threading.Event()
+        self._proc = None
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu),
-                                      f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            for line in self._proc.stdout:
+                line = line.strip()
+                if line:
+                    self.samples.append([x.strip() for x in line.split(",")])
+        except Exception:
+            pass
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
@@ -180,7 +191,8 @@ def run_nonsep(args):
             plan.nonsep(hi.alpha, out=out, stream=stream)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
-    ms = float(np.mean([s.elapsed_time(e) for s, e in evs]))
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    ms = float(np.mean(step_ms))
     k_ms = plan.kernel_ms()["nonsep"] / args.steps
     b_dev = out.cpu().numpy()
     plan.close()
@@ -196,7 +208,9 @@ def run_nonsep(args):
     achieved = exec_flops / (k_ms / 1e3) / 1e12
     line = {"metric": "Γ projection: (l-triple·x·mode) FP64 updates/s", "value": U / (ms / 1e3),
             "unit": "updates/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms, "ms_per_step_min": float(np.min(step_ms)),
+            "ms_per_step_median": float(np.median(step_ms)),
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config-3 inputs)",
             "config": {"workload": f"non-separable pointwise projection, BASELINE config 3: "
                                    f"{dom.count} sparse triples, Nx={spec.n_x}, {n} modes",

@@ -4,6 +4,7 @@
 // into MG_E* codes with a thread-local message (mg_last_error).  No CPU fallback exists:
 // without an sm_100 device the compute entry points return MG_ECUDA.
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <functional>
 #include <future>
@@ -51,9 +52,14 @@ DeviceGuard::DeviceGuard(int device) {
     MG_REQUIRE(device >= 0 && device < n, "device index out of range");
     MG_CUDA(cudaGetDevice(&prev));
     MG_CUDA(cudaSetDevice(device));
-    cudaDeviceProp prop;
-    MG_CUDA(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10) fail(MG_ECUDA, "library is built for sm_100a (B200) only");
+    // architecture check once per device (cudaGetDeviceProperties costs ~ms per call)
+    static std::atomic<int> checked[64];
+    if (device >= 64 || checked[device].load() == 0) {
+        int major = 0;
+        MG_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        if (major != 10) fail(MG_ECUDA, "library is built for sm_100a (B200) only");
+        if (device < 64) checked[device].store(1);
+    }
 }
 }  // namespace mg
 
