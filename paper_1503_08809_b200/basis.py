@@ -29,10 +29,14 @@ __all__ = [
 ]
 
 
-def _digest(*parts: bytes) -> str:
-    """16-hex-digit sha256 over the concatenated byte strings (basis.py:50-54)."""
+def _digest(*parts) -> str:
+    """16-hex-digit sha256 over the concatenated byte strings (basis.py:50-54).  Arrays are
+    hashed through a memoryview of their C-order buffer: the same bytes as `.tobytes()`
+    without the copy (120 MB of q̃ at config 1)."""
     h = hashlib.sha256()
     for part in parts:
+        if isinstance(part, np.ndarray):
+            part = memoryview(np.ascontiguousarray(part)).cast("B")
         h.update(part)
     return h.hexdigest()[:16]
 
@@ -71,7 +75,7 @@ class ModeMapping:
         return int(hit[0])
 
     def fingerprint(self) -> str:
-        return _digest(np.int64(self.p_max).tobytes(), self.entries.tobytes())
+        return _digest(np.int64(self.p_max).tobytes(), self.entries)
 
 
 def default_mode_mapping(p_max: int) -> ModeMapping:
@@ -101,7 +105,7 @@ class RadialGrid:
         return int(self.r.size)
 
     def fingerprint(self) -> str:
-        return _digest(self.r.tobytes())
+        return _digest(self.r)
 
 
 @dataclass(frozen=True)
@@ -142,7 +146,7 @@ class BasisTables:
         return np.arange(self.l_min, self.l_max + 1)
 
     def fingerprint(self) -> str:
-        return _digest(self.q.tobytes(), self.q_tilde.tobytes(), self.C.tobytes(),
+        return _digest(self.q, self.q_tilde, self.C,
                        self.v.tobytes(), np.int64([self.l_min, self.l_max]).tobytes())
 
 
