@@ -324,9 +324,10 @@ constexpr int PP_CHUNK = 16;  // pairs per block of the pair-product kernel
 #ifndef MG_PP_UNROLL
 #define MG_PP_UNROLL 2
 #endif
-// 128 threads x <= 32 registers: one warp per SM sub-partition, 1024 registers each, which
-// still fits beside a run-contraction CTA (17 warps x 96 registers leave one sub-partition
-// exactly 1024 free), so the side-stream pair products really run concurrently with it.
+// 128 threads x <= 32 registers: one warp per SM sub-partition, 1024 registers each (the
+// smallest footprint; with the 13-warp x 128-register run contraction no side CTA fits on
+// its fullest sub-partition, so the side stream mostly fills the contractions' tails —
+// capping the run contraction at 120 registers to make room was measured slower).
 __global__ void __maxnreg__(MG_PP_MAXREG)
 k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __restrict__ QT,
                 int p, int P2, int NxP, int l_min, double* __restrict__ S) {
