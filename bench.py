@@ -120,19 +120,47 @@ def dist_env():
 
 
 def total_updates(spec):
-    from paper_1503_08809_b200 import domain_count
-    T = domain_count(2, spec.l_max)
+    """(triples, updates per Γ, modes).  Counted with the oracle's C restatement of the
+    enumeration (oracle/domain_ref.c), so the reference arm never maps the product library."""
+    from oracle import ref
+    T = ref.domain_count(2, spec.l_max)
     n = (spec.p * (spec.p + 1) * (spec.p + 2)) // 6
     return T, T * spec.n_x * n, n
+
+
+def cpu_model() -> str:
+    """Host CPU model (lscpu "Model name") for the cpu_baseline record."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def native_maps() -> list:
+    """Shared objects of this repo mapped into the process (evidence for the arms)."""
+    try:
+        return sorted({ln.split()[-1] for ln in open("/proc/self/maps")
+                       if ln.rstrip().endswith(".so") and ROOT in ln})
+    except Exception:
+        return []
 
 
 # ------------------------------------------------------------------------------------------
 def cpu_rate(hi, qt_host, C, seconds, cores):
     """Oracle port (= reference _sweep_chunk code path) on a bounded flat slice, all cores."""
     from oracle import ref
-    from paper_1503_08809_b200 import domain_count
 
-    T = domain_count(2, hi.l_max)
+    T = ref.domain_count(2, hi.l_max)
     n = hi.entries.shape[0]
     per_core = 1.5e7                                  # upd/s/core, SURVEY §6 (c0..c4 slices)
     S = max(cores * 8, int(seconds * per_core * cores / (hi.x.size * n)))
@@ -244,6 +272,10 @@ def run_b200(args):
     world, rank, local = dist_env()
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
+    if world > 1:
+        # NCCL communicator lines (nranks, NVLS/P2P transport) stay visible in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     gloo = args.dist_backend == "gloo"
     backend_note = None
     if world > 1:
@@ -409,6 +441,7 @@ def run_b200(args):
         rate, S, a0, dt = cpu_rate(hi, qt_host, C, args.cpu_seconds, cores)
         line["cpu_baseline"] = {
             "value": rate, "unit": "updates/s", "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"oracle port of engine3d._sweep_chunk (B=64, fork pool of {cores}) over "
                       f"flat range [{a0}, {a0 + S}) of config {args.config[1:]} "
                       f"({S} triples, {dt:.1f} s); extrapolated s/Γ = {U / rate:.3g}"}
@@ -423,29 +456,27 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from multiprocessing import get_context
-
-    from oracle import qtilde_ref, ref
+    from oracle import ref
     from paper_1503_08809_b200.configs import CONFIGS, host_inputs
 
     spec = CONFIGS[args.config]
     hi = host_inputs(spec)
     T, U, nmodes = total_updates(spec)
     cores = os.cpu_count() or 1
-    per_core = 1.5e7
-    S = max(cores * 8, int(args.cpu_seconds * per_core * cores / (spec.n_x * nmodes)))
+    per_core = 1.0e7                                  # upd/s/core of the port (round-1 boxes)
+    # each step a bounded sample: the whole --warmup W --steps K run stays within ~3 minutes
+    step_s = min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup))
+    S = max(cores * 8, int(step_s * per_core * cores / (spec.n_x * nmodes)))
     S = min(S, T)
     a = T // 2
-    l1, l2, l3 = ref.domain_triples(2, spec.l_max, a, a + S)
-    ells = np.unique(np.concatenate([l1, l2, l3]))
-    d = qtilde_ref.delta_table(hi.k, hi.eps, 2, spec.l_max)
-    C = qtilde_ref.c_ell(d, hi.k, hi.wk)
-    chunks = np.array_split(ells, cores)
-    with get_context("fork").Pool(cores) as pool:
-        parts = pool.starmap(qtilde_ref.qtilde,
-                             [(hi.k, hi.wk, hi.x, hi.qk, d, 2, spec.l_max, list(c))
-                              for c in chunks])
-    qt = sum(parts)
+    # Table values do not change the port's operation count or memory traffic (no data-
+    # dependent branches, no denormals), so the reference arm times the port on seeded
+    # synthetic tables of the config's shapes instead of rebuilding q̃ with scipy (stage 1
+    # is not part of the reference, whose q̃ is an input; scipy at l ~ 2000 took minutes).
+    rng = np.random.default_rng(spec.seed)
+    L = spec.l_max - 1
+    qt = rng.standard_normal((spec.p, spec.n_x, L)) * 1e-10
+    C = rng.uniform(1e-5, 5e-2, L)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -457,7 +488,8 @@ def run_reference(args):
     rate = S * spec.n_x * nmodes / dt
     sample = (f"reference algorithm (NumPy restatement of engine3d._sweep_chunk, bit-identical "
               f"to cmbproj on config 0) over flat range [{a}, {a + S}) of config "
-              f"{args.config[1:]} ({S} triples), fork pool of {cores}, B=64")
+              f"{args.config[1:]} ({S} triples; seeded synthetic q̃/C of the config's shapes), fork "
+              f"pool of {cores}, B=64, on {cpu_model()}")
     line = {
         "metric": "Γ projection: (l-triple·x·mode) FP64 updates/s", "value": rate,
         "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -469,9 +501,10 @@ def run_reference(args):
         "impl": "reference",
         "s_per_gamma_extrapolated": U / rate,
         "cpu_baseline": {"value": rate, "unit": "updates/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": rate, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "native_so_loaded": native_maps(),
     }
     print(json.dumps(line), flush=True)
 

@@ -15,7 +15,8 @@
  *   - Return codes: MG_OK=0; MG_EINVAL=1 (-> ValueError); MG_ENOMEM=2 (-> MemoryError);
  *     MG_ECUDA=3 (-> RuntimeError, CLI exit code 3 per cli.py:142-145).  The message of the
  *     last failure on the calling thread is returned by mg_last_error().
- *   - Calls are synchronous and blocking (like the reference) and not re-entrant per device.
+ *   - Calls are synchronous and blocking (like the reference).  Calls from several host
+ *     threads are safe: executes on one device are serialised inside the library.
  *   - There is no CPU fallback: without a usable sm_100 device every compute entry point
  *     returns MG_ECUDA.
  */
@@ -60,6 +61,13 @@ int mg_domain_count(int l_min, int l_max, int64_t* count, int64_t* rows);
 int mg_domain_triples(int l_min, int l_max, int64_t begin, int64_t end, int32_t* l1,
                       int32_t* l2, int32_t* l3, int device);
 
+/* If (l1,l2,l3)[count] is exactly the flat range [b, b+count) of the reference enumeration,
+ * *begin = b; otherwise *begin = -1 (range detection for a user-built `domain` object,
+ * engine3d.py:170-171: a contiguous slice runs through mg_gamma_sep, anything else through
+ * mg_gamma_sep_triples).  One O(count) walk on the host, no device needed. */
+int mg_domain_match_range(int l_min, int l_max, const int32_t* l1, const int32_t* l2,
+                          const int32_t* l3, int64_t count, int64_t* begin);
+
 /* zm[t] = _triple_z(...) * permutation_multiplicity(...) for flat t in [begin,end)
  * (engine3d.py:41-53,133-134; geometry.py:114-142), computed on the device.
  * h2_mode = MG_H2_GOSPER is bit-identical to NumPy; MG_H2_EXACT agrees to a few ulp.
@@ -78,12 +86,18 @@ int mg_weights(int l_min, int l_max, const double* C, const double* v, int h2_mo
  *   modes [n][3]       mapping.entries, i<=j<=k<p (basis.py:57-75)
  *   [begin,end)        flat range of the reference enumeration (a _sweep_chunk range);
  *                      begin=0,end=-1 means the whole domain.
+ *   ndev, devs         the devices to shard over (devs NULL: 0..ndev-1; entries may repeat).
+ *                      Like the reference's `workers` fork pool (engine3d.py:175-186) the
+ *                      range is cut into ndev contiguous l2 slabs of equal modelled cost
+ *                      (the full domain: exactly the mg_slab_plan bounds), each computed on
+ *                      its device by its own host thread, and the partial Γ's are summed in
+ *                      slab order (merge_partials) — bitwise reproducible for a device list.
  *   gamma [n][n]       output, overwritten; rows = late modes n, cols = primordial n'
  *                      (gamma.py:14-16).
  * ------------------------------------------------------------------------------------- */
 int mg_gamma_sep(const double* q, const double* qt, const double* C, const double* v,
                  const double* wr2, const int64_t* modes, int p, int Nx, int n, int l_min,
-                 int l_max, int h2_mode, int64_t begin, int64_t end, int device,
+                 int l_max, int h2_mode, int64_t begin, int64_t end, int ndev, const int* devs,
                  double* gamma);
 
 /* Same, restricted to the (l2,l3)-rows whose l2 lies in [l2_begin,l2_end): the l2-slab
@@ -94,12 +108,13 @@ int mg_gamma_sep_slab(const double* q, const double* qt, const double* C, const 
                       int device, double* gamma);
 
 /* Same for an arbitrary explicit list of ordered valid triples (a user-built `domain`
- * object that is not a contiguous range, engine3d.py:170-171). */
+ * object that is not a contiguous range, engine3d.py:170-171); sharded over ndev devices by
+ * l2 slabs of the list like mg_gamma_sep. */
 int mg_gamma_sep_triples(const double* q, const double* qt, const double* C,
                          const double* v, const double* wr2, const int64_t* modes, int p,
                          int Nx, int n, int l_min, int l_max, int h2_mode,
                          const int32_t* l1, const int32_t* l2, const int32_t* l3,
-                         int64_t count, int device, double* gamma);
+                         int64_t count, int ndev, const int* devs, double* gamma);
 
 /* Balanced l2-slab boundaries for `nshards` ranks (cost model of the row-factorised kernel):
  * bounds[0..nshards] with bounds[0]=l_min, bounds[nshards]=l_max+1.  Host-only. */

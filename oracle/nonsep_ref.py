@@ -42,3 +42,41 @@ def nonsep(q, qt, C, v, wr2, entries, alpha, l_min, l1, l2, l3, W, h2_mode="gosp
             P += q1[cols[a]] * q2[cols[bb]] * q3[cols[c]]
         b += P @ (W[s:s + block] * zm * X)
     return b
+
+
+_SHARED = {}
+
+
+def _nonsep_job(args):
+    lo, hi, h2_mode, block = args
+    d = _SHARED
+    return nonsep(d["q"], d["qt"], d["C"], d["v"], d["wr2"], d["entries"], d["alpha"],
+                  d["l_min"], d["l1"][lo:hi], d["l2"][lo:hi], d["l3"][lo:hi], d["W"][lo:hi],
+                  h2_mode, block)
+
+
+def nonsep_parallel(q, qt, C, v, wr2, entries, alpha, l_min, l1, l2, l3, W, h2_mode="gosper",
+                    workers=None, block=256):
+    """`nonsep` over a fork pool: contiguous chunks, partials summed in worker order (the
+    reference's worker split, engine3d.py:175-186).  Inputs reach the workers through fork."""
+    import os
+    from multiprocessing import get_context
+
+    workers = workers or os.cpu_count() or 1
+    l1, l2, l3 = (np.asarray(a, np.int64) for a in (l1, l2, l3))
+    _SHARED.update(q=q, qt=qt, C=C, v=v, wr2=wr2, entries=entries, alpha=alpha, l_min=l_min,
+                   l1=l1, l2=l2, l3=l3, W=np.asarray(W, np.float64))
+    try:
+        bounds = np.linspace(0, l1.size, workers + 1).astype(np.int64)
+        jobs = [(int(a), int(b), h2_mode, block) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+        if len(jobs) <= 1:
+            parts = [_nonsep_job(j) for j in jobs]
+        else:
+            with get_context("fork").Pool(len(jobs)) as pool:
+                parts = pool.map(_nonsep_job, jobs)
+    finally:
+        _SHARED.clear()
+    out = np.zeros(entries.shape[0])
+    for p_ in parts:
+        out += p_
+    return out

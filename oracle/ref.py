@@ -124,16 +124,23 @@ def _log_fact(n: int) -> np.ndarray:
 
 
 def h2_exact(l1, l2, l3) -> np.ndarray:
-    """Racah closed form in the log-factorial domain (geometry.py:56-86), for valid
-    (triangle + even parity) triples only."""
-    a, b, c = (np.atleast_1d(np.asarray(x, np.int64)) for x in (l1, l2, l3))
+    """Racah closed form in the log-factorial domain (geometry.py:56-86); exactly 0 where
+    the triangle or even-parity condition fails (theta_indicator gate, geometry.py:44-54,
+    67-71)."""
+    a, b, c = np.broadcast_arrays(*(np.atleast_1d(np.asarray(x, np.int64))
+                                    for x in (l1, l2, l3)))
     L = a + b + c
-    g = L // 2
-    lf = _log_fact(int(L.max()) + 1)
-    log3j2 = (lf[L - 2 * a] + lf[L - 2 * b] + lf[L - 2 * c] - lf[L + 1]
-              + 2.0 * (lf[g] - lf[g - a] - lf[g - b] - lf[g - c]))
-    pref = (2 * a + 1) * (2 * b + 1) * (2 * c + 1) / (4.0 * np.pi)
-    return pref * np.exp(log3j2)
+    ok = (L % 2 == 0) & (c <= a + b) & (b <= a + c) & (a <= b + c)
+    out = np.zeros(a.shape)
+    if np.any(ok):
+        a, b, c, L = a[ok], b[ok], c[ok], L[ok]
+        g = L // 2
+        lf = _log_fact(int(L.max()) + 1)
+        log3j2 = (lf[L - 2 * a] + lf[L - 2 * b] + lf[L - 2 * c] - lf[L + 1]
+                  + 2.0 * (lf[g] - lf[g - a] - lf[g - b] - lf[g - c]))
+        pref = (2 * a + 1) * (2 * b + 1) * (2 * c + 1) / (4.0 * np.pi)
+        out[ok] = pref * np.exp(log3j2)
+    return out
 
 
 def triple_zm(l_min, l1, l2, l3, C, v, h2_mode="gosper") -> np.ndarray:
@@ -156,33 +163,95 @@ def triple_zm(l_min, l1, l2, l3, C, v, h2_mode="gosper") -> np.ndarray:
 # Γ port: _block_accumulate / _sweep_chunk / gamma3d_matrix (engine3d.py:86-186)
 # ----------------------------------------------------------------------------------------
 
-def block_accumulate(gamma, q, qt, entries, wr2, i1, i2, i3, zm):
-    """engine3d.py:86-120 — gamma += P X^T for one block of triples."""
-    cols = (entries[:, 0], entries[:, 1], entries[:, 2])
+def block_accumulate(gamma, q, qt, entries, wr2, i1, i2, i3, zm, cols=None):
+    """engine3d.py:86-120 — gamma += P X^T for one block of triples.  `cols` (test speed-up
+    at the largest configs) restricts X to a subset of the primordial modes: gamma is then
+    [n, len(cols)] and equals the full Γ[:, cols] (column n' of Γ only needs X[n'])."""
+    rows = (entries[:, 0], entries[:, 1], entries[:, 2])
+    xe = entries if cols is None else entries[np.asarray(cols)]
+    xcols = (xe[:, 0], xe[:, 1], xe[:, 2])
     q1, q2, q3 = q[:, i1], q[:, i2], q[:, i3]
     p_blk = np.zeros((entries.shape[0], i1.size))
     for a, b, c in _PERMS:
-        p_blk += q1[cols[a]] * q2[cols[b]] * q3[cols[c]]
+        p_blk += q1[rows[a]] * q2[rows[b]] * q3[rows[c]]
     t1, t2, t3 = qt[:, :, i1], qt[:, :, i2], qt[:, :, i3]
-    f = np.zeros((entries.shape[0], qt.shape[1], i1.size))
+    f = np.zeros((xe.shape[0], qt.shape[1], i1.size))
     for a, b, c in _PERMS:
-        f += t1[cols[a]] * t2[cols[b]] * t3[cols[c]]
+        f += t1[xcols[a]] * t2[xcols[b]] * t3[xcols[c]]
     x_blk = np.einsum("r,nrb->nb", wr2, f)
     x_blk *= zm
     gamma += p_blk @ x_blk.T
 
 
 def sweep_triples(q, qt, C, v, wr2, entries, l_min, l1, l2, l3, block=64,
-                  h2_mode="gosper"):
+                  h2_mode="gosper", cols=None):
     """engine3d.py:123-136 over an explicit triple list."""
     n = entries.shape[0]
-    gamma = np.zeros((n, n))
+    gamma = np.zeros((n, n if cols is None else len(cols)))
     for b0 in range(0, l1.size, block):
         b1 = min(b0 + block, l1.size)
         a, b, c = l1[b0:b1], l2[b0:b1], l3[b0:b1]
         zm = triple_zm(l_min, a, b, c, C, v, h2_mode)
-        block_accumulate(gamma, q, qt, entries, wr2, a - l_min, b - l_min, c - l_min, zm)
+        block_accumulate(gamma, q, qt, entries, wr2, a - l_min, b - l_min, c - l_min, zm, cols)
     return gamma
+
+
+_SHARED = {}
+
+
+def _triples_job(args):
+    lo, hi, block, h2_mode, cols = args
+    d = _SHARED
+    return sweep_triples(d["q"], d["qt"], d["C"], d["v"], d["wr2"], d["entries"], d["l_min"],
+                         d["l1"][lo:hi], d["l2"][lo:hi], d["l3"][lo:hi], block, h2_mode, cols)
+
+
+def sweep_triples_parallel(q, qt, C, v, wr2, entries, l_min, l1, l2, l3, workers=None,
+                           block=64, h2_mode="gosper", cols=None):
+    """sweep_triples over a fork pool (the reference's worker split, engine3d.py:175-186:
+    contiguous chunks, partials summed in worker order).  The inputs are shared with the
+    workers through fork, not pickled."""
+    workers = workers or os.cpu_count() or 1
+    l1, l2, l3 = (np.asarray(a, np.int64) for a in (l1, l2, l3))
+    _SHARED.update(q=q, qt=qt, C=C, v=v, wr2=wr2, entries=entries, l_min=l_min, l1=l1, l2=l2,
+                   l3=l3)
+    try:
+        bounds = np.linspace(0, l1.size, workers + 1).astype(np.int64)
+        jobs = [(int(a), int(b), block, h2_mode, cols) for a, b in zip(bounds[:-1], bounds[1:])
+                if b > a]
+        if len(jobs) <= 1:
+            parts = [_triples_job(j) for j in jobs]
+        else:
+            with get_context("fork").Pool(len(jobs)) as pool:
+                parts = pool.map(_triples_job, jobs)
+    finally:
+        _SHARED.clear()
+    if not parts:
+        return np.zeros((entries.shape[0], entries.shape[0] if cols is None else len(cols)))
+    out = parts[0].copy()
+    for p_ in parts[1:]:
+        out += p_
+    return out
+
+
+def slab_triples(l_min, l_max, l2_begin, l2_end):
+    """Every ordered valid triple whose l2 lies in [l2_begin, l2_end) (geometry.py:161-171
+    restricted to an l2 slab), ordered (l2, l3, l1).  Built directly, without enumerating the
+    domain: for each (l2, l3) row, l1 runs over max(l_min, l3 - l2) .. l2 with l1+l2+l3 even."""
+    out = [[], [], []]
+    for l2 in range(max(l2_begin, l_min), min(l2_end, l_max + 1)):
+        for l3 in range(l2, min(2 * l2, l_max) + 1):
+            lo = max(l_min, l3 - l2)
+            lo += (lo + l2 + l3) & 1
+            if lo > l2:
+                continue
+            l1 = np.arange(lo, l2 + 1, 2, dtype=np.int64)
+            out[0].append(l1)
+            out[1].append(np.full(l1.size, l2, np.int64))
+            out[2].append(np.full(l1.size, l3, np.int64))
+    if not out[0]:
+        return tuple(np.zeros(0, np.int64) for _ in range(3))
+    return tuple(np.concatenate(o) for o in out)
 
 
 def _sweep_job(args):

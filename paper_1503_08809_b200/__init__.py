@@ -13,7 +13,7 @@ There is no CPU fallback: compute calls raise if the CUDA library or the GPU is 
 from .basis import (BasisTables, ModeMapping, RadialGrid, default_mode_mapping,
                     shifted_legendre)
 from .engine3d import (DEFAULT_BLOCK, DomainRange, domain_count, domain_triples,
-                       gamma3d_matrix, triple_weights)
+                       gamma3d_matrix, resolve_devices, triple_weights)
 from .engine2d import PTable, build_ptable, gamma2d_matrix
 from .gamma import GammaMatrix
 from .gamma_io import (GammaFormatError, deserialize_gamma, load_checkpoint, merge_checkpoints,
@@ -31,6 +31,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BasisTables", "ModeMapping", "RadialGrid", "default_mode_mapping", "shifted_legendre",
     "DEFAULT_BLOCK", "DomainRange", "domain_count", "domain_triples", "gamma3d_matrix",
+    "resolve_devices",
     "triple_weights", "GammaMatrix", "SparseDomain", "gamma_nonsep", "GammaPlan",
     "bessel_table", "build_qtilde", "build_qtilde_device", "integration_weights", "x_weights",
     "ChunkPlan", "make_plan", "merge_partials", "slab_plan", "GammaFormatError",

@@ -31,13 +31,14 @@ _SIGS = {
     "mg_device_count": (_i, []),
     "mg_domain_count": (_i, [_i, _i, _vp, _vp]),
     "mg_domain_triples": (_i, [_i, _i, _i64, _i64, _vp, _vp, _vp, _i]),
+    "mg_domain_match_range": (_i, [_i, _i, _vp, _vp, _vp, _i64, _vp]),
     "mg_weights": (_i, [_i, _i, _vp, _vp, _i, _i64, _i64, _vp, _i]),
     "mg_gamma_sep": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i64, _i64, _i,
-                          _vp]),
+                          _vp, _vp]),
     "mg_gamma_sep_slab": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i,
                                _vp]),
     "mg_gamma_sep_triples": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp,
-                                  _vp, _i64, _i, _vp]),
+                                  _vp, _i64, _i, _vp, _vp]),
     "mg_slab_plan": (_i, [_i, _i, _i, _i, _i, _vp]),
     "mg_plan_create": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
     "mg_plan_create_dev": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp]),

@@ -9,6 +9,7 @@
 #include <functional>
 #include <future>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mg_common.cuh"
@@ -89,6 +90,68 @@ static void full_range_bounds(const DomainIndex& D, int64_t begin, int64_t end, 
     D.triple(end, e[0], e[1], e[2]);
 }
 
+// Cost model of one (l2,l3)-row with an l1 window of m triples (scheduler.py slab_costs,
+// calibrated on a B200: the run contraction pays ~20 padded l1 per row, per-row work outside
+// the run contraction is ~1.35x the x contraction).
+static inline double row_cost(double m, int p, int Nx) {
+    const double pairs = p * (p + 1) / 2.0;
+    return (double)p * p * Nx * (m + 20.0) + 1.35 * pairs * p * p * Nx;
+}
+
+// Balanced contiguous l2 slabs of the full domain: bounds[0] = l_min .. bounds[n] = l_max+1
+// (mg_slab_plan; the shard plan of both the torchrun ranks and the multi-device call).
+static std::vector<int> slab_bounds(int l_min, int l_max, int p, int Nx, int nshards) {
+    std::vector<double> cum(l_max - l_min + 2, 0.0);
+    for (int l2 = l_min; l2 <= l_max; ++l2) {
+        double c = 0;
+        for (int l3 = l2; l3 <= std::min(2 * l2, l_max); ++l3) {
+            int par = (l2 + l3) & 1;
+            int lo = std::max(l_min, l3 - l2);
+            if ((lo & 1) != par) ++lo;
+            int hi = (l2 & 1) == par ? l2 : l2 - 1;
+            if (lo > hi) continue;
+            c += row_cost((hi - lo) / 2 + 1, p, Nx);
+        }
+        cum[l2 - l_min + 1] = cum[l2 - l_min] + c;
+    }
+    std::vector<int> bounds(nshards + 1);
+    bounds[0] = l_min;
+    for (int s = 1; s < nshards; ++s) {
+        double target = cum.back() * s / nshards;
+        int idx = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        bounds[s] = std::max(bounds[s - 1], std::min(l_min + idx, l_max + 1));
+    }
+    bounds[nshards] = l_max + 1;
+    return bounds;
+}
+
+// Balanced l2 cut points for an arbitrary row list (flat sub-range or explicit triples):
+// per-l2 modelled cost of the rows actually present, cut at the first l2 whose preceding
+// cost reaches each target.  Returns bounds as above.
+static std::vector<int> row_bounds(const std::vector<MgRow>& rows, int l_min, int l_max, int p,
+                                   int Nx, int nshards) {
+    std::vector<double> cum(l_max - l_min + 2, 0.0);
+    for (const MgRow& r : rows) cum[r.l2 - l_min + 1] += row_cost(r.jhi - r.jlo + 1, p, Nx);
+    for (size_t i = 1; i < cum.size(); ++i) cum[i] += cum[i - 1];
+    std::vector<int> bounds(nshards + 1);
+    bounds[0] = l_min;
+    for (int s = 1; s < nshards; ++s) {
+        double target = cum.back() * s / nshards;
+        int idx = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        bounds[s] = std::max(bounds[s - 1], std::min(l_min + idx, l_max + 1));
+    }
+    bounds[nshards] = l_max + 1;
+    return bounds;
+}
+
+static std::vector<int> device_list(int ndev, const int* devs) {
+    MG_REQUIRE(ndev >= 1 && ndev <= 64, "ndev must be in [1, 64]");
+    std::vector<int> d(ndev);
+    for (int i = 0; i < ndev; ++i) d[i] = devs ? devs[i] : i;
+    return d;
+}
+
+
 extern "C" {
 
 int mg_version(void) { return 100; }
@@ -126,6 +189,45 @@ int mg_domain_triples(int l_min, int l_max, int64_t begin, int64_t end, int32_t*
         MG_REQUIRE(l1 && l2 && l3, "null output");
         DeviceGuard g(device);
         weights(l_min, l_max, nullptr, nullptr, 0, begin, end, nullptr, l1, l2, l3);
+    });
+}
+
+int mg_domain_match_range(int l_min, int l_max, const int32_t* l1, const int32_t* l2,
+                          const int32_t* l3, int64_t count, int64_t* begin) {
+    return guarded([&] {
+        MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
+        MG_REQUIRE(begin && count >= 0, "invalid argument");
+        MG_REQUIRE(count == 0 || (l1 && l2 && l3), "null triple arrays");
+        *begin = -1;
+        if (count == 0) {
+            *begin = 0;
+            return;
+        }
+        int a = l1[0], b = l2[0], c = l3[0];
+        if (a < l_min || a > l_max || b < a || b > l_max) return;
+        const int st = row_start(a, b), n = row_len(a, b, l_max);
+        if (n <= 0 || c < st || ((c - st) & 1) || (c - st) / 2 >= n) return;
+        DomainIndex D;
+        D.build(l_min, l_max);
+        const int64_t flat0 = D.row_base[D.pair_off[a - l_min] + (b - a)] + (c - st) / 2;
+        if (flat0 + count > D.count) return;
+        // walk the enumeration order (geometry.py:161-171) alongside the list
+        for (int64_t i = 1; i < count; ++i) {
+            c += 2;
+            if (c > std::min(a + b, l_max)) {
+                for (++b;; ++b) {
+                    if (b > l_max) {
+                        ++a;
+                        b = a;
+                        if (a > l_max) return;  // unreachable: flat0 + count <= D.count
+                    }
+                    if (row_len(a, b, l_max) > 0) break;
+                }
+                c = row_start(a, b);
+            }
+            if (l1[i] != a || l2[i] != b || l3[i] != c) return;
+        }
+        *begin = flat0;
     });
 }
 
@@ -280,28 +382,84 @@ static void gamma_common(const double* q, const double* qt, const double* C, con
     MG_CUDA(cudaMemcpy(gamma, P.gamma.p, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost));
 }
 
+// Run one shard per entry of `devs`, each on its own host thread with its own plan on its
+// device (q̃ uploaded to every device, like the reference's per-worker copies), then merge the
+// partial Γ's in shard order — merge_partials (scheduler.py:48-66) — so the result is bitwise
+// reproducible for a given device list.  Shards on the same device serialise through the
+// device's execute lock (device_mutex).  `run(P, s)` executes shard s on plan P.
+static void gamma_shards(const double* q, const double* qt, const double* C, const double* v,
+                         const double* wr2, const int64_t* modes, int p, int Nx, int n,
+                         int l_min, int l_max, int h2_mode, const std::vector<int>& devs,
+                         double* gamma, const std::function<void(mg_plan*, int)>& run) {
+    const int ns = (int)devs.size();
+    if (ns == 1) {
+        gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, devs[0], gamma,
+                     [&](mg_plan* P) { run(P, 0); });
+        return;
+    }
+    MG_REQUIRE(gamma, "null argument");
+    const size_t nn = (size_t)n * n;
+    std::vector<std::vector<double>> parts(ns);
+    std::vector<std::exception_ptr> errs(ns);
+    std::vector<std::thread> th;
+    for (int s = 0; s < ns; ++s)
+        th.emplace_back([&, s] {
+            try {
+                parts[s].assign(nn, 0.0);
+                gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, devs[s],
+                             parts[s].data(), [&](mg_plan* P) { run(P, s); });
+            } catch (...) {
+                errs[s] = std::current_exception();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    std::memcpy(gamma, parts[0].data(), nn * sizeof(double));
+    for (int s = 1; s < ns; ++s)
+        for (size_t i = 0; i < nn; ++i) gamma[i] += parts[s][i];
+}
+
 int mg_gamma_sep(const double* q, const double* qt, const double* C, const double* v,
                  const double* wr2, const int64_t* modes, int p, int Nx, int n, int l_min,
-                 int l_max, int h2_mode, int64_t begin, int64_t end, int device,
+                 int l_max, int h2_mode, int64_t begin, int64_t end, int ndev, const int* devs,
                  double* gamma) {
     return guarded([&] {
         MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
-        // The rows of the flat range are enumerated on a host thread while the plan uploads
-        // and transposes q̃ (the one-shot drop-in call pays both every time).
-        std::vector<MgRow> rows;
-        auto host_rows = std::async(std::launch::async, [&] {
+        const std::vector<int> dv = device_list(ndev, devs);
+        // The rows of the flat range are enumerated on a host thread while the plans upload
+        // and transpose q̃ (the one-shot drop-in call pays both every time), then cut into
+        // one l2-slab shard per device: the full domain with the mg_slab_plan bounds (so the
+        // shards are exactly the torchrun ranks' slabs), a sub-range with the same cost model
+        // over its rows.
+        std::vector<std::vector<MgRow>> shard(dv.size());
+        std::shared_future<void> host_rows = std::async(std::launch::async, [&] {
             DomainIndex D;
             D.build(l_min, l_max);
             const int64_t e_ = end < 0 ? D.count : end;
             int s[3], e[3];
             full_range_bounds(D, begin, e_, s, e);
+            std::vector<MgRow> rows;
             if (begin < e_) build_rows_range(l_min, l_max, l_min, l_max + 1, s, e, rows);
+            const int nsh = (int)dv.size();
+            if (nsh == 1) {
+                shard[0] = std::move(rows);
+                return;
+            }
+            const std::vector<int> b = (begin == 0 && e_ == D.count)
+                                           ? slab_bounds(l_min, l_max, p, Nx, nsh)
+                                           : row_bounds(rows, l_min, l_max, p, Nx, nsh);
+            for (const MgRow& r : rows) {
+                int k = (int)(std::upper_bound(b.begin(), b.end(), r.l2) - b.begin()) - 1;
+                shard[std::min(std::max(k, 0), nsh - 1)].push_back(r);
+            }
         });
-        gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, device, gamma,
-                     [&](mg_plan* P) {
-                         host_rows.get();  // rethrows a range error from the host thread
-                         execute_rows(P, std::move(rows), 0);
+        gamma_shards(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, dv, gamma,
+                     [&](mg_plan* P, int s) {
+                         host_rows.wait();
+                         execute_rows(P, std::move(shard[s]), 0);
                      });
+        host_rows.get();  // rethrows a range error from the host thread
     });
 }
 
@@ -321,11 +479,48 @@ int mg_gamma_sep_triples(const double* q, const double* qt, const double* C,
                          const double* v, const double* wr2, const int64_t* modes, int p,
                          int Nx, int n, int l_min, int l_max, int h2_mode,
                          const int32_t* l1, const int32_t* l2, const int32_t* l3,
-                         int64_t count, int device, double* gamma) {
+                         int64_t count, int ndev, const int* devs, double* gamma) {
     return guarded([&] {
         MG_REQUIRE(count == 0 || (l1 && l2 && l3), "null triple arrays");
-        gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, device, gamma,
-                     [&](mg_plan* P) { execute_triples(P, l1, l2, l3, count, 0); });
+        MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
+        const std::vector<int> dv = device_list(ndev, devs);
+        const int ns = (int)dv.size();
+        if (ns == 1) {
+            gamma_common(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, dv[0], gamma,
+                         [&](mg_plan* P) { execute_triples(P, l1, l2, l3, count, 0); });
+            return;
+        }
+        // l2-slab shards of the explicit list, balanced by the per-l2 row cost model
+        std::vector<MgRow> rows;
+        {
+            std::vector<std::pair<int, int>> keys((size_t)count);
+            for (int64_t i = 0; i < count; ++i) {
+                MG_REQUIRE(l2[i] >= l_min && l2[i] <= l_max, "triple outside [l_min, l_max]");
+                keys[i] = {l2[i], l3[i] * 2 + (l1[i] & 1)};
+            }
+            std::sort(keys.begin(), keys.end());
+            for (size_t i = 0; i < keys.size();) {
+                size_t j = i;
+                while (j < keys.size() && keys[j] == keys[i]) ++j;
+                MgRow r{keys[i].first, 0, 0, 0, (int)(j - i) - 1, 0};
+                rows.push_back(r);
+                i = j;
+            }
+        }
+        const std::vector<int> b = row_bounds(rows, l_min, l_max, p, Nx, ns);
+        std::vector<std::vector<int32_t>> s1(ns), s2(ns), s3(ns);
+        for (int64_t i = 0; i < count; ++i) {
+            int k = (int)(std::upper_bound(b.begin(), b.end(), l2[i]) - b.begin()) - 1;
+            k = std::min(std::max(k, 0), ns - 1);
+            s1[k].push_back(l1[i]);
+            s2[k].push_back(l2[i]);
+            s3[k].push_back(l3[i]);
+        }
+        gamma_shards(q, qt, C, v, wr2, modes, p, Nx, n, l_min, l_max, h2_mode, dv, gamma,
+                     [&](mg_plan* P, int s) {
+                         execute_triples(P, s1[s].data(), s2[s].data(), s3[s].data(),
+                                         (int64_t)s1[s].size(), 0);
+                     });
     });
 }
 
@@ -333,30 +528,8 @@ int mg_slab_plan(int l_min, int l_max, int p, int Nx, int nshards, int* bounds) 
     return guarded([&] {
         MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
         MG_REQUIRE(nshards >= 1 && bounds, "invalid shard count");
-        const double pairs = p * (p + 1) / 2.0;
-        std::vector<double> cum(l_max - l_min + 2, 0.0);
-        for (int l2 = l_min; l2 <= l_max; ++l2) {
-            double c = 0;
-            for (int l3 = l2; l3 <= std::min(2 * l2, l_max); ++l3) {
-                int par = (l2 + l3) & 1;
-                int lo = std::max(l_min, l3 - l2);
-                if ((lo & 1) != par) ++lo;
-                int hi = (l2 & 1) == par ? l2 : l2 - 1;
-                if (lo > hi) continue;
-                double m = (hi - lo) / 2 + 1;
-                // calibrated model (scheduler.py slab_costs): run contraction pays ~20 padded
-                // l1 per row; per-row work is ~1.35x the x contraction
-                c += (double)p * p * Nx * (m + 20.0) + 1.35 * pairs * p * p * Nx;
-            }
-            cum[l2 - l_min + 1] = cum[l2 - l_min] + c;
-        }
-        bounds[0] = l_min;
-        for (int s = 1; s < nshards; ++s) {
-            double target = cum.back() * s / nshards;
-            int idx = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
-            bounds[s] = std::max(bounds[s - 1], std::min(l_min + idx, l_max + 1));
-        }
-        bounds[nshards] = l_max + 1;
+        std::vector<int> b = slab_bounds(l_min, l_max, p, Nx, nshards);
+        std::copy(b.begin(), b.end(), bounds);
     });
 }
 

@@ -120,11 +120,15 @@ __device__ __forceinline__ double zm_gosper(int l1, int l2, int l3, const double
 }
 
 // h2_exact via a log-factorial table lf[] (geometry.py:73-85), then the same prefactor.
+// Like the reference (theta_indicator gate, geometry.py:44-54,67-71) the weight is exactly 0
+// where the triangle or even-parity condition fails — the sparse config-3 domain and explicit
+// triple lists may contain such triples, and the log-factorial indices are invalid there.
 __device__ __forceinline__ double zm_exact(int l1, int l2, int l3, const double* __restrict__ C,
                                            const double* __restrict__ v, int l_min,
                                            const double* __restrict__ lf) {
     const double four_pi = 4.0 * 3.141592653589793;
     int L = l1 + l2 + l3, g = L / 2;
+    if ((L & 1) || l3 > l1 + l2 || l2 > l1 + l3 || l1 > l2 + l3) return 0.0;
     double s = __dsub_rn(__dadd_rn(__dadd_rn(lf[L - 2 * l1], lf[L - 2 * l2]), lf[L - 2 * l3]),
                          lf[L + 1]);
     double t = __dsub_rn(__dsub_rn(__dsub_rn(lf[g], lf[g - l1]), lf[g - l2]), lf[g - l3]);

@@ -23,6 +23,7 @@
 #include <mutex>
 #include <type_traits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -442,25 +443,69 @@ k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int n
     }, smem);
 }
 
-// second x-contraction tile (chosen for p = 30): 120 x 96 on 12 consumer warps (5x3
-// fragments each, 120 registers, no spills).  Measured at config 4: 1 % faster than 160 x 96
-// on 12 warps (5x4 fragments, spills 60 B) and 3 % faster than 160 x 96 on 16 warps
-// (96-register cap, spills); M = 465 pads to 480 in both.
-using CfgX160 = TileCfg<3, 4, 5, 3>;
-using CfgX128 = TileCfg<2, 4, 8, 4>;   // 128 x 128, 8 consumer warps (p = 22)
+// x-contraction tiles.  The CTA tile is chosen per basis size from M = p(p+1)/2 pairs and
+// N = p^2 (c,c') columns (choose_xtile).  Consumer warps are 12 (3 per SM sub-partition: every
+// DMMA unit serves the same number of warps; 13 warps allocate up to 128 registers) or 15
+// (120 x 120, p = 15, where no 12-warp tiling of M = 120 fits N = 225 better):
+//   T120     120 x 120, 15 warps, 3x5 fragments              p = 15: M exact, N 225 -> 240
+//   T120x96  120 x 96,  12 warps, 5x3 fragments              (round 1's p = 30 tile)
+//   T128x72  128 x 72,  12 warps, 4x3 fragments              p = 22: 253 x 484 -> 256 x 504
+//   T160x72  160 x 72,  12 warps, 5x3 fragments              p = 30: 465 x 900 -> 480 x 936
+//   T128     128 x 128,  8 warps, 8x4 fragments (spills)     kept for A/B measurements
+// Measured in round 1 (ncu): the 8-warp 128 x 128 tile at p = 22 ran the DMMA pipe at 78 %
+// (168 registers with local-memory spills); the 12-warp 120 x 96 tile at p = 30 at 96 %.
+using CfgX120x96 = TileCfg<3, 4, 5, 3>;
+using CfgX128x72 = TileCfg<4, 3, 4, 3>;
+using CfgX160x72 = TileCfg<4, 3, 5, 3>;
+using CfgX128 = TileCfg<2, 4, 8, 4>;
 
-// Tile choice for the x contraction: padded-area efficiency of M = p(p+1)/2, N = p^2, times
-// the sub-partition balance of the consumer warps (15 warps leave one of the four SMSPs with
-// three: at most 15/16 of the DMMA units busy).
-enum class XTile { T120, T160, T128 };
+enum class XTile { T120 = 0, T120x96, T128x72, T160x72, T128, COUNT };
+
+// Padded-area efficiency of M = P2, N = pp on a bm x bn tile, times a per-tile pipe factor
+// (sub-partition balance / measured DMMA-pipe utilisation).  MG_XTILE=<index> forces a tile
+// (A/B measurements).
 static XTile choose_xtile(int P2, int pp) {
-    auto eff = [&](int bm, int bn, double bal) {
-        return bal * (double)P2 * pp / ((double)ceil_div(P2, bm) * bm * ceil_div(pp, bn) * bn);
-    };
-    const double e120 = eff(120, 120, 15.0 / 16.0), e160 = eff(CfgX160::BM, CfgX160::BN, 1.0),
-                 e128 = eff(128, 128, 1.0);
-    if (e120 >= e160 && e120 >= e128) return XTile::T120;
-    return e160 >= e128 ? XTile::T160 : XTile::T128;
+    if (const char* f = std::getenv("MG_XTILE")) {
+        const int i = std::atoi(f);
+        if (i >= 0 && i < (int)XTile::COUNT) return (XTile)i;
+    }
+    struct Cand { XTile t; int bm, bn; double pipe; };
+    const Cand cands[] = {{XTile::T120, 120, 120, 15.0 / 16.0},
+                          {XTile::T120x96, CfgX120x96::BM, CfgX120x96::BN, 1.0},
+                          {XTile::T128x72, CfgX128x72::BM, CfgX128x72::BN, 1.0},
+                          {XTile::T160x72, CfgX160x72::BM, CfgX160x72::BN, 1.0},
+                          {XTile::T128, 128, 128, 0.8}};
+    XTile best = XTile::T120;
+    double be = -1.0;
+    for (const Cand& c : cands) {
+        const double e = c.pipe * (double)P2 * pp /
+                         ((double)ceil_div(P2, c.bm) * c.bm * ceil_div(pp, c.bn) * c.bn);
+        if (e > be + 1e-9) { be = e; best = c.t; }
+    }
+    return best;
+}
+
+template <class Cfg>
+static void launch_x(int num_sms, cudaStream_t st, const double* S, const double* H, int nrows,
+                     int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* G) {
+    k_x_contract_p<Cfg><<<num_sms, XPipeP<Cfg>::THREADS, XPipeP<Cfg>::smem_bytes, st>>>(
+        S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G);
+}
+template <class Cfg>
+static void attr_x() {
+    MG_CUDA(cudaFuncSetAttribute(k_x_contract_p<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)XPipeP<Cfg>::smem_bytes));
+}
+static void launch_xtile(XTile xt, int num_sms, cudaStream_t st, const double* S, const double* H,
+                         int nrows, int row_b1, int row_b3, int p, int P2, int Nx, int NxP,
+                         double* G) {
+    switch (xt) {
+        case XTile::T120: launch_x<CfgX120>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
+        case XTile::T120x96: launch_x<CfgX120x96>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
+        case XTile::T128x72: launch_x<CfgX128x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
+        case XTile::T160x72: launch_x<CfgX160x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
+        default: launch_x<CfgX128>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -740,6 +785,21 @@ MgScratch* scratch_pool(int device) {
     return pools[device].get();
 }
 
+// Every plan on a device shares that device's scratch (MgScratch).  Executes are serialised
+// per device by holding this lock across the host-side enqueue: each pipeline starts by
+// waiting on the legacy stream 0 and ends by making stream 0 wait for it, so on the GPU the
+// next execute's use of the scratch (and any reallocation by ensure(), stream-ordered on
+// stream 0) starts only after the previous one finished.  Recursive: execute_triples may
+// delegate to execute_rows.
+std::recursive_mutex& device_mutex(int device) {
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<std::recursive_mutex>> locks;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)locks.size() <= device) locks.resize(device + 1);
+    if (!locks[device]) locks[device].reset(new std::recursive_mutex());
+    return *locks[device];
+}
+
 // Batch geometry: K1/K2 work on nb1 rows at a time (H buffer), K3 on nb3 (G buffer).
 static void choose_batches(mg_plan* P) {
     // Scratch per row: H (run contraction out), S (pair products), G (x contraction out),
@@ -936,21 +996,14 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     bool& attr_done = attr_done_dev[P->device & 63];
     const size_t smem_run = RunPipeP::smem_bytes;
     const XTile xt = choose_xtile(P2, pp);
-    const size_t smem_x = xt == XTile::T120   ? XPipeP<CfgX120>::smem_bytes
-                          : xt == XTile::T160 ? XPipeP<CfgX160>::smem_bytes
-                                              : XPipeP<CfgX128>::smem_bytes;
     if (!attr_done) {
         MG_CUDA(cudaFuncSetAttribute(k_run_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_run));
-        MG_CUDA(cudaFuncSetAttribute(k_x_contract_p<CfgX120>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)XPipeP<CfgX120>::smem_bytes));
-        MG_CUDA(cudaFuncSetAttribute(k_x_contract_p<CfgX160>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)XPipeP<CfgX160>::smem_bytes));
-        MG_CUDA(cudaFuncSetAttribute(k_x_contract_p<CfgX128>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)XPipeP<CfgX128>::smem_bytes));
+        attr_x<CfgX120>();
+        attr_x<CfgX120x96>();
+        attr_x<CfgX128x72>();
+        attr_x<CfgX160x72>();
+        attr_x<CfgX128>();
         MG_CUDA(cudaFuncSetAttribute(k_pair_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_run));
         attr_done = true;
@@ -1070,16 +1123,8 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         MG_CUDA(cudaStreamWaitEvent(ms, P->ev_s, 0));
 #endif
         prof_mark(P, 2, ms);
-        if (xt == XTile::T120) {
-            k_x_contract_p<CfgX120><<<num_sms, XPipeP<CfgX120>::THREADS, smem_x, ms>>>(
-                P->sc->S.p, P->sc->H.p, nb, (int)B.b1, (int)B.b3, p, P2, P->Nx, NxP, P->sc->G.p);
-        } else if (xt == XTile::T160) {
-            k_x_contract_p<CfgX160><<<num_sms, XPipeP<CfgX160>::THREADS, smem_x, ms>>>(
-                P->sc->S.p, P->sc->H.p, nb, (int)B.b1, (int)B.b3, p, P2, P->Nx, NxP, P->sc->G.p);
-        } else {
-            k_x_contract_p<CfgX128><<<num_sms, XPipeP<CfgX128>::THREADS, smem_x, ms>>>(
-                P->sc->S.p, P->sc->H.p, nb, (int)B.b1, (int)B.b3, p, P2, P->Nx, NxP, P->sc->G.p);
-        }
+        launch_xtile(xt, num_sms, ms, P->sc->S.p, P->sc->H.p, nb, (int)B.b1, (int)B.b3, p, P2,
+                     P->Nx, NxP, P->sc->G.p);
         MG_LAUNCHED();
         MG_CUDA(cudaEventRecord(P->ev_x, ms));
         launches += 4 + (dt1 ? 1 : 0);
@@ -1142,6 +1187,7 @@ static void set_rows(mg_plan* P, std::vector<MgRow>&& rows) {
 }
 
 void execute_rows(mg_plan* P, std::vector<MgRow>&& rows, cudaStream_t st) {
+    std::lock_guard<std::recursive_mutex> lock(device_mutex(P->device));
     set_rows(P, std::move(rows));
     if (P->prep.hrows.empty()) return zero_result(P, st);
     run_pipeline(P, P->prep.hrows, P->prep.hzoff, st, nullptr, nullptr, nullptr, nullptr,
@@ -1151,6 +1197,7 @@ void execute_rows(mg_plan* P, std::vector<MgRow>&& rows, cudaStream_t st) {
 // l2 slab [l2a, l2b) of the full domain; the batch tables are reused when the same slab is
 // executed again on this plan (bench steps, multi-GPU ranks).
 void execute_slab(mg_plan* P, int l2a, int l2b, cudaStream_t st) {
+    std::lock_guard<std::recursive_mutex> lock(device_mutex(P->device));
     MgPrepared& pre = P->prep;
     if (!(pre.valid && pre.key_a == l2a && pre.key_b == l2b)) {
         int s[3] = {P->l_min, 0, 0}, e[3] = {P->l_max + 1, 0, 0};
@@ -1167,6 +1214,7 @@ void execute_slab(mg_plan* P, int l2a, int l2b, cudaStream_t st) {
 
 void execute_triples(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
                      int64_t count, cudaStream_t st) {
+    std::lock_guard<std::recursive_mutex> lock(device_mutex(P->device));
     const int lmin = P->l_min, lmax = P->l_max;
     struct T { int l2, l3, par, l1; };
     std::vector<T> ts;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 #include "mg_common.cuh"
@@ -24,8 +25,8 @@ constexpr int MG_NPROF = 8;
 
 // Batch scratch, pooled per device so that one-shot calls (the drop-in API) do not pay for
 // allocating and zeroing gigabytes every time.  Buffers only grow; they are zeroed when
-// (re)allocated (H's x pads must never hold NaN) and never shrink.  Plans on one device are
-// not re-entrant (documented in include/modal_b200.h), so sharing is safe.
+// (re)allocated (H's x pads must never hold NaN) and never shrink.  Executes on one device
+// are serialised by device_mutex(), so concurrent callers (threads, shards) share it safely.
 struct MgScratch {
     mg::DBuf<double> ZT, panel, H, S, G, R, Sq, Z;
 };
@@ -105,6 +106,7 @@ struct mg_plan {
 
 namespace mg {
 MgScratch* scratch_pool(int device);
+std::recursive_mutex& device_mutex(int device);
 void plan_init(mg_plan* P, const double* q, const double* qt_host, const double* qt_dev,
                const double* C, const double* v, const double* wr2, const int64_t* modes,
                int p, int Nx, int n, int l_min, int l_max, int h2_mode);

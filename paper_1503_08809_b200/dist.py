@@ -16,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as nat
-from .engine3d import _base_meta
+from .engine3d import _base_meta, check_shapes
 from .gamma import GammaMatrix
 from .quadrature import x_weights
 from .scheduler import slab_plan
@@ -52,6 +52,7 @@ def slab_partial(tables, mapping, wr2, l2_begin, l2_end, h2_mode="gosper", devic
     v = np.ascontiguousarray(tables.v, np.float64)
     e = np.ascontiguousarray(mapping.entries, np.int64)
     wr2 = np.ascontiguousarray(wr2, np.float64)
+    check_shapes(q, qt, C, v, wr2, int(tables.l_min), int(tables.l_max))
     n = e.shape[0]
     out = np.zeros((n, n))
     nat.check(nat.lib().mg_gamma_sep_slab(
@@ -78,7 +79,9 @@ def gamma3d_matrix_distributed(tables, mapping, grid, h2_mode="gosper", integrat
     wr2 = x_weights(grid.r, integrator)
     a, b = rank_slab(int(tables.l_min), int(tables.l_max), tables.p_max, wr2.size, rank, world)
     if partial_fn is None:
-        dev = rank if device is None else device
+        import os
+        # the rank's own GPU on its node (LOCAL_RANK), never the global rank
+        dev = int(os.environ.get("LOCAL_RANK", "0")) if device is None else int(device)
         part = slab_partial(tables, mapping, wr2, a, b, h2_mode, dev)
         use_cuda = dist.get_backend(group) == "nccl"
         t = torch.from_numpy(part)

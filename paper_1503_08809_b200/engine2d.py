@@ -58,6 +58,8 @@ def build_ptable(tables, grid, rule, legendre, budget_bytes: int = DEFAULT_PTABL
     if need > budget_bytes:
         raise MemoryError(f"P table needs {need} bytes but the budget allows {budget_bytes}")
     q, qt, lw, leg = _inputs(tables, legendre)
+    if np.size(grid.r) != nr:
+        raise ValueError(f"radial grid has {np.size(grid.r)} points but q_tilde has {nr}")
     out = np.zeros((p, p, nr, nmu))
     nat.check(nat.lib().mg_ptable(nat.ptr(q), nat.ptr(qt), nat.ptr(lw), nat.ptr(leg), p, nr,
                                   lw.size, nmu, int(device), nat.ptr(out)))
@@ -71,6 +73,8 @@ def gamma2d_matrix(tables, mapping, grid, rule, legendre, integrator: str = "tra
     e = np.ascontiguousarray(mapping.entries, np.int64)
     n = e.shape[0]
     wr2 = np.ascontiguousarray(x_weights(grid.r, integrator))
+    if wr2.size != nr:
+        raise ValueError(f"radial grid has {wr2.size} points but q_tilde has {nr} (n_radial)")
     muw = np.ascontiguousarray(rule.weights, np.float64)
     out = np.zeros((n, n))
     if ptable is not None:

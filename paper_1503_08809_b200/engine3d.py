@@ -1,7 +1,7 @@
 """Drop-in replacement for `cmbproj.gamma3d_matrix` (engine3d.py:156-186).
 
     gamma3d_matrix(tables, mapping, grid, h2_mode="gosper", integrator="trap", block=64,
-                   workers=1, domain=None, *, device=None) -> GammaMatrix
+                   workers=1, domain=None, *, device=None, devices=None) -> GammaMatrix
 
 Same signature, argument meaning, errors and `meta` keys as the reference; a user switches
 by rebinding the name (harness.py:21 imports it at module level, which is how the
@@ -9,8 +9,9 @@ reference's own tests swap engines, test_harness.py:278-279) — see INTEGRATION
 
 Differences that do not change results:
   * `block` and `workers` are validated and recorded in `meta` like the reference does, but
-    the device path has its own tiling; `workers` CPU processes become one GPU (or the
-    ranks of `paper_1503_08809_b200.dist`).
+    the device path has its own tiling; the reference's `workers` fork pool becomes the
+    visible GPUs (`devices`, one l2-slab shard per GPU, partials merged in order), or the
+    ranks of `paper_1503_08809_b200.dist` under torchrun.
   * `domain` may be the reference's TriangularDomain (or any object with l1/l2/l3/count), a
     `DomainRange` (a contiguous flat range, never materialised), or None (whole domain).
     A domain that is a contiguous flat range of the full enumeration runs through the
@@ -27,7 +28,7 @@ from . import _native as nat
 from .gamma import GammaMatrix
 from .quadrature import x_weights
 
-__all__ = ["gamma3d_matrix", "DomainRange", "DEFAULT_BLOCK", "domain_count",
+__all__ = ["gamma3d_matrix", "resolve_devices", "DomainRange", "DEFAULT_BLOCK", "domain_count",
            "domain_triples", "triple_weights"]
 
 DEFAULT_BLOCK = 64
@@ -104,6 +105,22 @@ def triple_weights(C, v, l_min: int, l_max: int, begin: int = 0, end: int | None
     return out
 
 
+def check_shapes(q, qt, C, v, wr2, l_min: int, l_max: int) -> None:
+    """Shape agreement of the host arrays handed to the C-ABI (which reads p*L, p*Nx*L, L and
+    Nx doubles through raw pointers).  The reference fails the same inputs with a ValueError
+    from its einsum (engine3d.py:117) or its BasisTables validation (basis.py:232-246)."""
+    L = int(l_max) - int(l_min) + 1
+    if q.ndim != 2 or q.shape[1] != L:
+        raise ValueError(f"q must have shape (p, {L}), got {q.shape}")
+    if qt.ndim != 3 or qt.shape[0] != q.shape[0] or qt.shape[2] != L:
+        raise ValueError(f"q_tilde must have shape ({q.shape[0]}, Nx, {L}), got {qt.shape}")
+    if C.shape != (L,) or v.shape != (L,):
+        raise ValueError(f"C and v must have shape ({L},)")
+    if wr2.shape != (qt.shape[1],):
+        raise ValueError(f"radial grid has {wr2.size} points but q_tilde has "
+                         f"{qt.shape[1]} (n_radial)")
+
+
 def _base_meta(tables, grid, mapping, integrator, h2_mode, block, workers):
     """Provenance keys of engine3d.py:139-153,172-174."""
     return _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers,
@@ -138,32 +155,42 @@ def _as_range(domain, l_min, l_max):
     return None
 
 
-def _flat_index_of_first(l1, l2, l3, l_min, l_max):
-    """Flat index of triple (l1,l2,l3) in the reference order (for range detection)."""
-    n = 0
-    for a in range(l_min, l1):
-        for b in range(a, l_max + 1):
-            start = b if a % 2 == 0 else b + 1
-            stop = min(a + b, l_max)
-            n += 0 if start > stop else (stop - start) // 2 + 1
-    for b in range(l1, l2):
-        start = b if l1 % 2 == 0 else b + 1
-        stop = min(l1 + b, l_max)
-        n += 0 if start > stop else (stop - start) // 2 + 1
-    start = l2 if l1 % 2 == 0 else l2 + 1
-    return n + (l3 - start) // 2
+def resolve_devices(device=None, devices=None) -> list[int]:
+    """Devices a one-shot call shards over, in order of precedence:
+    `devices` (sequence) > `device` (int) > env MG_DEVICES ("0,1,2,3") > under torchrun
+    (WORLD_SIZE > 1) the rank's own LOCAL_RANK > every visible device.  Entries may repeat
+    (two shards on one GPU run one after the other)."""
+    import os
+    if devices is not None:
+        out = [int(d) for d in devices]
+    elif device is not None:
+        out = [int(device)]
+    elif os.environ.get("MG_DEVICES"):
+        out = [int(d) for d in os.environ["MG_DEVICES"].split(",") if d.strip()]
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        out = [int(os.environ.get("LOCAL_RANK", "0"))]
+    else:
+        out = list(range(max(1, nat.lib().mg_device_count())))
+    if not out or len(out) > 64:
+        raise ValueError("need between 1 and 64 devices")
+    return out
 
 
 def gamma3d_matrix(tables, mapping, grid, h2_mode: str = "gosper", integrator: str = "trap",
                    block: int = DEFAULT_BLOCK, workers: int = 1, domain=None, *,
-                   device: int | None = None) -> GammaMatrix:
-    """Γ[n, n'] = Σ_t zm_t P[n,t] X[n',t] on the GPU (see module docstring)."""
+                   device: int | None = None, devices=None) -> GammaMatrix:
+    """Γ[n, n'] = Σ_t zm_t P[n,t] X[n',t] on the GPU (see module docstring).
+
+    `device` / `devices` choose the GPU(s) (see `resolve_devices`; default: every visible
+    GPU).  With several devices the domain is cut into l2 slabs of equal modelled cost, one
+    per device, and the partial Γ's are summed in slab order — the reference's fork pool +
+    merge_partials (engine3d.py:175-186) with GPUs for workers, inside the unchanged call.
+    `meta["devices"]` records the list."""
     if block < 1:                                              # engine3d.py:168-169
         raise ValueError("block must be >= 1")
     if h2_mode not in nat.MG_H2:                               # engine3d.py:53
         raise ValueError(f"unknown h2_mode {h2_mode!r}")
-    if device is None:
-        device = 0
+    devs = np.ascontiguousarray(resolve_devices(device, devices), np.int32)
     q = np.ascontiguousarray(tables.q, np.float64)
     qt = np.ascontiguousarray(tables.q_tilde, np.float64)
     C = np.ascontiguousarray(tables.C, np.float64)
@@ -174,19 +201,22 @@ def gamma3d_matrix(tables, mapping, grid, h2_mode: str = "gosper", integrator: s
     wr2 = np.ascontiguousarray(x_weights(grid.r, integrator), np.float64)
     p, nx, n = q.shape[0], qt.shape[1], entries.shape[0]
     l_min, l_max = int(tables.l_min), int(tables.l_max)
+    check_shapes(q, qt, C, v, wr2, l_min, l_max)
     # The sha256 fingerprints of the inputs (meta, engine3d.py:139-153) cost ~0.25 s for a
     # config-1 q̃; hashlib and the ctypes call both release the GIL, so they overlap.
     fp = _FP_POOL.submit(lambda: (tables.fingerprint(), grid.fingerprint(),
                                   mapping.fingerprint()))
 
     def meta():
-        return _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers,
-                          *fp.result())
+        m = _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers, *fp.result())
+        m["devices"] = devs.tolist()
+        return m
 
     out = np.zeros((n, n))
     lib = nat.lib()
     common = (nat.ptr(q), nat.ptr(qt), nat.ptr(C), nat.ptr(v), nat.ptr(wr2), nat.ptr(entries),
               p, nx, n, l_min, l_max, nat.MG_H2[h2_mode])
+    shards = (int(devs.size), nat.ptr(devs))
     rng = _as_range(domain, l_min, l_max)
     if rng is None:
         l1 = np.ascontiguousarray(np.asarray(domain.l1), np.int32)
@@ -195,24 +225,18 @@ def gamma3d_matrix(tables, mapping, grid, h2_mode: str = "gosper", integrator: s
         rng = _detect_contiguous(l1, l2, l3, l_min, l_max)
         if rng is None:
             nat.check(lib.mg_gamma_sep_triples(*common, nat.ptr(l1), nat.ptr(l2), nat.ptr(l3),
-                                               int(l1.size), int(device), nat.ptr(out)))
+                                               int(l1.size), *shards, nat.ptr(out)))
             return GammaMatrix(out, meta())
     begin, end = rng
     if end > begin:
-        nat.check(lib.mg_gamma_sep(*common, int(begin), int(end), int(device), nat.ptr(out)))
+        nat.check(lib.mg_gamma_sep(*common, int(begin), int(end), *shards, nat.ptr(out)))
     return GammaMatrix(out, meta())
 
 
 def _detect_contiguous(l1, l2, l3, l_min, l_max):
-    """If the triple arrays are exactly flat range [b, e) of the enumeration, return it."""
-    n = l1.size
-    if n == 0:
-        return (0, 0)
-    b = _flat_index_of_first(int(l1[0]), int(l2[0]), int(l3[0]), l_min, l_max)
-    total = domain_count(l_min, l_max)
-    if b + n > total:
-        return None
-    r1, r2, r3 = domain_triples(l_min, l_max, b, b + n)
-    if np.array_equal(r1, l1) and np.array_equal(r2, l2) and np.array_equal(r3, l3):
-        return (b, b + n)
-    return None
+    """(b, e) if the int32 triple arrays are exactly flat range [b, e) of the enumeration
+    (one host-side O(n) walk in the C library, no device enumeration), else None."""
+    b = np.zeros(1, np.int64)
+    nat.check(nat.lib().mg_domain_match_range(int(l_min), int(l_max), nat.ptr(l1), nat.ptr(l2),
+                                              nat.ptr(l3), int(l1.size), nat.ptr(b)))
+    return None if b[0] < 0 else (int(b[0]), int(b[0]) + int(l1.size))

@@ -5,8 +5,9 @@ Restates the reference's serialisation (harness.py:183-250) byte for byte:
        "%.17g" values joined by ","
   bin  b"MGAM" + u32 version(1) + u32 rows + u32 cols (little endian) + row-major <f8 payload
 Checkpoints: a flat-range (or l2-slab) partial Γ is saved as MGAM plus a JSON sidecar with
-its range and provenance; `merge_checkpoints` adds partials in the given order (the analogue
-of merge_partials, scheduler.py:48-66), so an interrupted Γ restarts from its missing ranges.
+its range and provenance; `merge_checkpoints` adds disjoint partials in span order (the
+analogue of merge_partials, scheduler.py:48-66) and can require exact coverage, so an
+interrupted Γ restarts from its missing ranges and is never merged with a hole or overlap.
 """
 
 from __future__ import annotations
@@ -103,8 +104,24 @@ def load_checkpoint(path):
     return g, side
 
 
-def merge_checkpoints(paths) -> GammaMatrix:
-    """Sum partial checkpoints in the given order; refuses mismatched inputs."""
+def _span(side):
+    """(kind, start, stop) of a checkpoint sidecar: a flat range or an l2 slab (or None)."""
+    for kind, key in (("range", "range"), ("l2_slab", "l2_slab")):
+        b, e = (side.get(key) or [None, None])[:2]
+        if b is not None and e is not None:
+            return kind, int(b), int(e)
+    return None
+
+
+def merge_checkpoints(paths, *, expect=None) -> GammaMatrix:
+    """Sum partial checkpoints (the analogue of merge_partials, scheduler.py:48-66).
+
+    Refuses mismatched inputs (shape, input fingerprints).  Partials that record their span
+    (flat range or l2 slab, see `save_checkpoint`) are summed in span order and must be
+    disjoint; `expect=(start, stop)` additionally requires them to tile [start, stop) exactly
+    (e.g. (0, domain_count(l_min, l_max)) for flat ranges or (l_min, l_max + 1) for l2 slabs),
+    so an interrupted Γ is never silently merged with a hole or a double-counted range.
+    Partials without a recorded span are summed in the given order (no coverage check)."""
     parts = [load_checkpoint(p) for p in paths]
     if not parts:
         raise ValueError("no checkpoints")
@@ -113,9 +130,29 @@ def merge_checkpoints(paths) -> GammaMatrix:
         if g.shape != head.shape or any(g.meta.get(k) != head.meta.get(k)
                                         for k in ("tables", "grid", "mapping")):
             raise ValueError("checkpoints have mismatched shape or input fingerprints")
-    acc = head.values.copy()
+    spans = [_span(side) for _, side in parts]
+    if any(s is not None for s in spans):
+        if any(s is None for s in spans) or len({s[0] for s in spans}) != 1:
+            raise ValueError("checkpoints mix flat ranges, l2 slabs and unranged partials")
+        order = sorted(range(len(parts)), key=lambda i: (spans[i][1], spans[i][2]))
+        for a, b in zip(order[:-1], order[1:]):
+            if spans[b][1] < spans[a][2]:
+                raise ValueError(f"checkpoint spans overlap: {spans[a][1:]} and {spans[b][1:]}")
+        if expect is not None:
+            lo, hi = int(expect[0]), int(expect[1])
+            cur = lo
+            for i in order:
+                if spans[i][1] != cur:
+                    raise ValueError(f"checkpoints leave [{cur}, {spans[i][1]}) uncovered")
+                cur = spans[i][2]
+            if cur != hi:
+                raise ValueError(f"checkpoints leave [{cur}, {hi}) uncovered")
+        parts = [parts[i] for i in order]
+    elif expect is not None:
+        raise ValueError("checkpoints record no span: coverage cannot be checked")
+    acc = parts[0][0].values.copy()
     for g, _ in parts[1:]:
         acc += g.values
-    meta = dict(head.meta)
+    meta = dict(parts[0][0].meta)
     meta["workers_merged"] = len(parts)
     return GammaMatrix(acc, meta)

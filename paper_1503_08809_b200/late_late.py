@@ -32,10 +32,11 @@ def gamma_late_late(tables, mapping, h2_mode: str = "gosper", *,
     e = np.ascontiguousarray(mapping.entries, np.int64)
     n = e.shape[0]
     out = np.zeros((n, n))
+    devs = np.array([device], np.int32)
     nat.check(nat.lib().mg_gamma_sep(
         nat.ptr(q), nat.ptr(qt), nat.ptr(C), nat.ptr(v), nat.ptr(wr2), nat.ptr(e), q.shape[0],
-        1, n, int(tables.l_min), int(tables.l_max), nat.MG_H2[h2_mode], 0, -1, int(device),
-        nat.ptr(out)))
+        1, n, int(tables.l_min), int(tables.l_max), nat.MG_H2[h2_mode], 0, -1, 1,
+        nat.ptr(devs), nat.ptr(out)))
     meta = {"engine": "modal3d-QQ", "l_min": tables.l_min, "l_max": tables.l_max,
             "p_max": tables.p_max, "n_max": n, "h2_mode": h2_mode,
             "tables": tables.fingerprint(), "mapping": mapping.fingerprint()}

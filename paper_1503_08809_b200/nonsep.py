@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from .engine3d import _FP_POOL, _meta_dict
+from .engine3d import _FP_POOL, _meta_dict, check_shapes
 from .gamma import GammaMatrix
 from .quadrature import x_weights
 
@@ -63,6 +63,7 @@ def gamma_nonsep(tables, mapping, grid, alpha, domain: SparseDomain, h2_mode: st
     if alpha.shape != (entries.shape[0],):
         raise ValueError("alpha must have one coefficient per primordial mode")
     wr2 = np.ascontiguousarray(x_weights(grid.r, integrator), np.float64)
+    check_shapes(q, qt, C, v, wr2, int(tables.l_min), int(tables.l_max))
     l1 = np.ascontiguousarray(domain.l1, np.int32)
     l2 = np.ascontiguousarray(domain.l2, np.int32)
     l3 = np.ascontiguousarray(domain.l3, np.int32)

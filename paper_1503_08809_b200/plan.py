@@ -31,6 +31,12 @@ class GammaPlan:
         self.n = self.entries.shape[0]
         self.nx = self.wr2.size
         self._h = ctypes.c_void_p()
+        L = self.l_max - self.l_min + 1
+        if tuple(q_tilde.shape) != (self.p, self.nx, L):
+            raise ValueError(f"q_tilde must have shape ({self.p}, {self.nx}, {L}) to match q "
+                             f"and wr2, got {tuple(q_tilde.shape)}")
+        if self.q.shape != (self.p, L) or self.C.shape != (L,) or self.v.shape != (L,):
+            raise ValueError("q, C, v do not match [l_min, l_max]")
         lib = nat.lib()
         args = (nat.ptr(self.q), None, nat.ptr(self.C), nat.ptr(self.v), nat.ptr(self.wr2),
                 nat.ptr(self.entries), self.p, self.nx, self.n, self.l_min, self.l_max,

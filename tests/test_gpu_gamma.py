@@ -392,3 +392,60 @@ class TestEdgeCases:
             got = gamma3d_matrix(t, m, r, domain=DomainRange(3, 25, a, b)).values
             want = ref.gamma3d(t.q, t.q_tilde, t.C, t.v, x_weights(r.r), m.entries, 3, 25, a, b)
             assert frob_rel(got, want) < 1e-12
+
+
+class TestMultiDevice:
+    """gamma3d_matrix over several devices inside the unchanged call (engine3d.py:175-186's
+    fork pool with GPUs for workers).  One GPU here, so the shards are `devices=[0, 0]`: the
+    host threads, the per-shard plans, the l2-slab split and the ordered merge all run; the
+    shards serialise on the device's execute lock."""
+
+    def test_full_domain_two_shards_c0(self, g_c0):
+        from paper_1503_08809_b200 import slab_plan
+        hi = host_inputs("c0")
+        t = BasisTables(hi.q, g_c0["qt"], g_c0["C"], hi.v, 2, 200)
+        m, r = ModeMapping(hi.entries, 6), RadialGrid(hi.x)
+        one = gamma3d_matrix(t, m, r, devices=[0])
+        two = gamma3d_matrix(t, m, r, devices=[0, 0])
+        assert two.meta["devices"] == [0, 0] and one.meta["devices"] == [0]
+        b = slab_plan(2, 200, 6, hi.x.size, 2)
+        plan = GammaPlan.from_tables(t, m, r)
+        parts = []
+        for a, e in zip(b[:-1], b[1:]):
+            plan.execute(a, e)
+            parts.append(plan.fetch())
+        want = parts[0].copy()
+        want += parts[1]
+        assert np.array_equal(two.values, want)             # = the two-slab sum, bitwise
+        assert frob_rel(two.values, one.values) < 1e-12
+        assert frob_rel(two.values, g_c0["gamma"]) < 1e-10
+
+    def test_full_domain_four_shards_c1(self, c1):
+        hi, C, qt = c1
+        t = BasisTables(hi.q, qt, C, hi.v, 2, hi.l_max)
+        m, r = ModeMapping(hi.entries, hi.spec.p), RadialGrid(hi.x)
+        one = gamma3d_matrix(t, m, r, devices=[0]).values
+        four = gamma3d_matrix(t, m, r, devices=[0, 0, 0, 0]).values
+        assert frob_rel(four, one) < 1e-12
+        again = gamma3d_matrix(t, m, r, devices=[0, 0, 0, 0]).values
+        assert np.array_equal(four, again)                   # reproducible per device list
+
+    def test_subrange_and_triples_sharded(self, g_c0):
+        hi = host_inputs("c0")
+        t = BasisTables(hi.q, g_c0["qt"], g_c0["C"], hi.v, 2, 200)
+        m, r = ModeMapping(hi.entries, 6), RadialGrid(hi.x)
+        d = DomainRange(2, 200, 1000, 20000)
+        got = gamma3d_matrix(t, m, r, domain=d, devices=[0, 0, 0]).values
+        assert frob_rel(got, g_c0["partial_1000_20000"]) < 1e-10
+        l1, l2, l3 = ref.domain_triples(2, 200)
+        keep = (np.arange(l1.size) % 5) != 2
+
+        class Dom:
+            pass
+
+        dd = Dom()
+        dd.l1, dd.l2, dd.l3 = l1[keep], l2[keep], l3[keep]
+        dd.count = int(keep.sum())
+        a = gamma3d_matrix(t, m, r, domain=dd, devices=[0]).values
+        b = gamma3d_matrix(t, m, r, domain=dd, devices=[0, 0]).values
+        assert frob_rel(b, a) < 1e-12

@@ -53,10 +53,13 @@ class TestStage1:
         den = np.linalg.norm(ref, axis=(0, 1))
         assert np.max(num / den) < 1e-11                      # per-l relative Frobenius
 
-    def test_c1_sampled_l(self):
-        hi = host_inputs("c1")
+    @pytest.mark.parametrize("cfg,ells", [("c1", [2, 3, 500, 1499, 1998, 2000]),
+                                          ("c2", [2, 1251, 2499, 2500]),
+                                          ("c4", [2, 1501, 2999, 3000])])
+    def test_sampled_l(self, cfg, ells):
+        """Sampled multipoles at p = 15 / 22 / 30, Nk 3000 / 4000 / 5000, kx up to 6000."""
+        hi = host_inputs(cfg)
         C, qt = build_qtilde(hi)
-        ells = [2, 3, 500, 1499, 1998, 2000]
         d = qtilde_ref.delta_table(hi.k, hi.eps, 2, hi.l_max)
         Cr = qtilde_ref.c_ell(d, hi.k, hi.wk)
         assert np.max(np.abs(C / Cr - 1)) < 1e-11

@@ -51,6 +51,26 @@ class TestABI:
         with pytest.raises(RuntimeError, match="no CUDA device"):
             mg.triple_weights(np.ones(3), np.ones(3), 2, 4)
 
+    @pytest.mark.parametrize("lmin,lmax", [(2, 40), (3, 25), (2, 200), (4, 4), (2, 2)])
+    def test_range_detection(self, lmin, lmax):
+        """mg_domain_match_range (host walk of the enumeration): contiguous flat ranges are
+        recognised with their start, anything with a hole or out of order is not."""
+        from oracle import ref
+        from paper_1503_08809_b200.engine3d import _detect_contiguous
+        T = ref.domain_count(lmin, lmax)
+        for a, b in {(0, T), (0, 1), (min(5, T - 1), T), (T - 1, T),
+                     (min(17, T - 1), min(123, T)), (T // 2, min(T // 2 + 1000, T))}:
+            l1, l2, l3 = (x.astype(np.int32) for x in ref.domain_triples(lmin, lmax, a, b))
+            assert _detect_contiguous(l1, l2, l3, lmin, lmax) == (a, b)
+            if b - a > 2:
+                k = np.ones(b - a, bool)
+                k[(b - a) // 2] = False
+                assert _detect_contiguous(l1[k], l2[k], l3[k], lmin, lmax) is None
+                r = [np.ascontiguousarray(x[::-1]) for x in (l1, l2, l3)]
+                assert _detect_contiguous(*r, lmin, lmax) is None
+        bad = np.array([lmax + 1], np.int32)
+        assert _detect_contiguous(bad, bad, bad, lmin, lmax) is None
+
     def test_slab_plan_matches_python(self):
         b = np.zeros(9, np.int32)
         for spec in CONFIGS.values():
@@ -159,3 +179,23 @@ class TestConfigs:
         want = ref.domain_triples(2, 30)
         assert np.array_equal(l1, want[0]) and np.array_equal(l2, want[1])
         assert np.array_equal(l3, want[2]) and np.all(W == 1.0)
+
+
+def test_device_selection(monkeypatch):
+    """Device list of the one-shot call: devices > device > MG_DEVICES > LOCAL_RANK under
+    torchrun > every visible device."""
+    from paper_1503_08809_b200 import resolve_devices
+    monkeypatch.delenv("MG_DEVICES", raising=False)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    assert resolve_devices(None, [1, 0]) == [1, 0]
+    assert resolve_devices(3, None) == [3]
+    monkeypatch.setenv("MG_DEVICES", "0,0")
+    assert resolve_devices() == [0, 0]
+    monkeypatch.delenv("MG_DEVICES")
+    monkeypatch.setenv("WORLD_SIZE", "8")
+    monkeypatch.setenv("LOCAL_RANK", "5")
+    assert resolve_devices() == [5]
+    monkeypatch.delenv("WORLD_SIZE")
+    assert resolve_devices() == [0]                          # no GPU here: one (failing) device
+    with pytest.raises(ValueError):
+        resolve_devices(None, [])

@@ -70,3 +70,29 @@ def test_checkpoints_merge_in_order(tmp_path):
     save_checkpoint(other, tmp_path / "bad.mgam")
     with pytest.raises(ValueError):
         merge_checkpoints([paths[0], tmp_path / "bad.mgam"])
+
+
+def test_checkpoint_spans_are_validated(tmp_path):
+    rng = np.random.default_rng(2)
+    g = [GammaMatrix(rng.standard_normal((4, 4)), dict(META)) for _ in range(3)]
+    paths = []
+    for i, (b, e) in enumerate(((20, 35), (0, 20), (35, 50))):    # saved out of order
+        p = tmp_path / f"c{i}.mgam"
+        save_checkpoint(g[i], p, begin=b, end=e)
+        paths.append(p)
+    merged = merge_checkpoints(paths, expect=(0, 50))
+    want = g[1].values.copy()
+    want += g[0].values
+    want += g[2].values                                              # summed in span order
+    assert np.array_equal(merged.values, want)
+    with pytest.raises(ValueError, match="uncovered"):
+        merge_checkpoints(paths[:2], expect=(0, 50))                 # hole [35, 50)
+    dup = tmp_path / "dup.mgam"
+    save_checkpoint(g[0], dup, begin=30, end=40)
+    with pytest.raises(ValueError, match="overlap"):
+        merge_checkpoints(paths + [dup])
+    slab = tmp_path / "slab.mgam"
+    save_checkpoint(g[0], slab, l2_begin=2, l2_end=10)
+    with pytest.raises(ValueError, match="mix"):
+        merge_checkpoints([paths[0], slab])
+    assert np.array_equal(merge_checkpoints([slab], expect=(2, 10)).values, g[0].values)
