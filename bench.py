@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-reps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="config 3: run the CPU restatement over ALL sparse triples")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: exchange Γ partials through host memory (lets N ranks share "
                          "one GPU for testing the multi-rank path; never for measurements)")
@@ -234,6 +236,42 @@ def run_nonsep(args):
         e2e.append(time.perf_counter() - t0)
     e2e_s = float(np.median(e2e))
     achieved = exec_flops / (k_ms / 1e3) / 1e12
+    if p <= 8 and not os.environ.get("MG_NS_DFMA"):
+        kname = f"k_nonsep_dmma<{4 if p <= 4 else 8}>"
+        knote = ("FP64 tensor pipe: the Ã·S contraction (M = p) on DMMA.8x8x4, pair products "
+                 "and the l1/x reductions on DFMA (same FP64 datapath, peak shared)")
+    else:
+        kname = f"k_nonsep_warp<{p}>"
+        knote = "DFMA-pipe bound pointwise kernel"
+
+    # CPU baseline: the restatement (oracle/nonsep_ref.py, gamma3d_naive's loop structure)
+    # on a strided sample of the sparse triples (or all of them with --cpu-full), with all
+    # host cores; the GPU result over the same sub-domain is checked against it.
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import nonsep_ref
+        cores = os.cpu_count() or 1
+        per_core = 1.0e7                                 # upd/s/core of the restatement
+        S = dom.count if args.cpu_full else min(
+            dom.count, max(cores * 64, int(args.cpu_seconds * per_core * cores / (spec.n_x * n))))
+        idx = np.unique(np.linspace(0, dom.count - 1, S).astype(np.int64))
+        sub = SparseDomain(dom.l1[idx], dom.l2[idx], dom.l3[idx], dom.weight[idx])
+        t0 = time.perf_counter()
+        b_cpu = nonsep_ref.nonsep_parallel(hi.q, qt, C, hi.v, hi.wr2, hi.entries, hi.alpha, 2,
+                                           sub.l1, sub.l2, sub.l3, sub.weight, workers=cores)
+        dt = time.perf_counter() - t0
+        b_gpu = b.values[:, 0] if idx.size == dom.count else \
+            gamma_nonsep(t, m, grid, hi.alpha, sub).values[:, 0]
+        err = float(np.linalg.norm(b_gpu - b_cpu) / np.linalg.norm(b_cpu))
+        cpu = {"value": idx.size * spec.n_x * n / dt, "unit": "updates/s", "cores": cores,
+               "kind": "port", "cpu_model": cpu_model(),
+               "sample": (f"oracle/nonsep_ref.nonsep_parallel (gamma3d_naive loop structure) "
+                          f"over {'ALL' if idx.size == dom.count else 'a strided sample of'} "
+                          f"{idx.size} of {dom.count} sparse triples, fork pool of {cores}, "
+                          f"{dt:.1f} s; GPU b over the same triples: rel err {err:.2e} "
+                          f"(tolerance 1e-8)"),
+               "rel_err_vs_gpu": err, "s": dt}
+        assert err <= 1e-8, f"non-separable GPU/CPU mismatch {err:.3e}"
     line = {"metric": "Γ projection: (l-triple·x·mode) FP64 updates/s", "value": U / (ms / 1e3),
             "unit": "updates/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "ms_per_step_min": float(np.min(step_ms)),
@@ -244,12 +282,12 @@ def run_nonsep(args):
                                    f"{dom.count} sparse triples, Nx={spec.n_x}, {n} modes",
                        "updates_per_step": U,
                        "l2_flush": "256 MiB write between timed steps (untimed)"},
-            "roofline": {"bound": "tensor", "kernel": "k_nonsep_warp", "achieved": achieved,
+            "roofline": {"bound": "tensor", "kernel": kname, "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
                          "executed_flops_per_tx": exec_per_tx,
-                         "note": "DFMA-pipe bound (no DMMA form: the sum is pointwise per "
-                                 "(triple, x)); executed FLOPs / kernel time",
+                         "note": knote + "; executed FLOPs (3 P2 + 2 p P2 + 2 p + 2 per "
+                                 "(triple, x)) / kernel time (CUDA events on the stream)",
                          "kernel_ms_per_step": k_ms},
             "e2e": {"value": U / e2e_s, "unit": "updates/s",
                     "h2d_bytes_per_step": int(qt.nbytes + hi.q.nbytes + dom.count * 20),
@@ -259,6 +297,8 @@ def run_nonsep(args):
                     "note": "timed through the public gamma_nonsep call with host buffers"},
             "gpu_launches": 2,
             "b_norm": float(np.linalg.norm(b.values)), "clocks": clk.summary()}
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
 
 
@@ -452,10 +492,60 @@ def run_b200(args):
 
 
 # ------------------------------------------------------------------------------------------
+def run_reference_nonsep(args):
+    """Reference arm at config 3: the restatement of the non-separable path (gamma3d_naive's
+    loop structure, oracle/nonsep_ref.py) on a strided sample of the sparse triples per step,
+    all host cores, seeded synthetic q̃/C of the config's shapes."""
+    from oracle import nonsep_ref
+    from paper_1503_08809_b200.configs import CONFIGS, host_inputs, sparse_domain, sparse_grid
+
+    spec = CONFIGS[args.config]
+    hi = host_inputs(spec)
+    l1, l2, l3, W = sparse_domain(*sparse_grid(l_max=spec.l_max))
+    n = hi.entries.shape[0]
+    cores = os.cpu_count() or 1
+    step_s = min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup))
+    S = min(l1.size, max(cores * 64, int(step_s * 1.0e7 * cores / (spec.n_x * n))))
+    idx = np.unique(np.linspace(0, l1.size - 1, S).astype(np.int64))
+    rng = np.random.default_rng(spec.seed)
+    qt = rng.standard_normal((spec.p, spec.n_x, spec.l_max - 1)) * 1e-10
+    C = rng.uniform(1e-5, 5e-2, spec.l_max - 1)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        nonsep_ref.nonsep_parallel(hi.q, qt, C, hi.v, hi.wr2, hi.entries, hi.alpha, 2, l1[idx],
+                                   l2[idx], l3[idx], W[idx], workers=cores)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    rate = idx.size * spec.n_x * n / dt
+    sample = (f"non-separable restatement (gamma3d_naive loop structure) over a strided sample "
+              f"of {idx.size} of {l1.size} config-3 sparse triples per step (seeded synthetic "
+              f"q̃/C of the config's shapes), fork pool of {cores}, on {cpu_model()}")
+    line = {
+        "metric": "Γ projection: (l-triple·x·mode) FP64 updates/s", "value": rate,
+        "unit": "updates/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config shapes)",
+        "config": {"workload": f"non-separable pointwise projection, BASELINE config 3 (strided "
+                               f"sample per step)", "updates_per_step": idx.size * spec.n_x * n,
+                   "parallelism": f"cpu x{cores}"},
+        "impl": "reference",
+        "cpu_baseline": {"value": rate, "unit": "updates/s", "cores": cores, "kind": "port",
+                         "cpu_model": cpu_model(), "sample": sample},
+        "e2e": {"value": rate, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "native_so_loaded": native_maps(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    if args.config == "c3":
+        return run_reference_nonsep(args)
     from oracle import ref
     from paper_1503_08809_b200.configs import CONFIGS, host_inputs
 

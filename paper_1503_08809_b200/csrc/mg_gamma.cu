@@ -1556,6 +1556,187 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int nblocks, 
     out[i] = s;
 }
 
+// ------------------------------------------------------------------------------------------
+// DMMA form of the pointwise kernel (p <= 8; config 3 has p = 8).  The dominant term of the
+// pointwise bispectrum, T[c][(t,x)] = Σ_{a<=b} Ã[c][ab] S_ab(t,x) (576 of the 702 FLOPs per
+// (triple, x) at p = 8), is an [8 x 36] x [36 x (t,x)] GEMM with M = p: the m8n8k4 DMMA
+// shape, with Ã as the (constant) A operand held in registers for the whole kernel.
+//
+// The B operand is built in registers, no shared memory: for a chunk of 8 x columns, lane
+// (g, t4) owns column x0 + g and k-slot t4 of every k-step, i.e. it must produce S_ab for a
+// pair (a, b) that depends on t4.  The K order makes those register indices compile-time:
+// the 36 unordered pairs of Z_PP are grouped by cyclic difference d = b - a (mod PP) into
+// groups of 4 consecutive rotations {(r, r+d) : r = i0..i0+3}, and lane t4 holds its q̃
+// components ROTATED by t4 (register i = component (i + t4) mod PP, read from a table whose
+// component axis is stored twice so that i + t4 never wraps).  Pair (i0 + t4, i0 + d + t4)
+// is then registers (i0, (i0 + d) mod PP) in every lane: 9 k-steps at PP = 8, no padding.
+//   rotations r < PP/2 only for d = PP/2 (r and r + PP/2 are the same pair);
+//   p < PP: components >= p are zero in the tables and the Ã fragments.
+// C fragment: lane holds T[c = g][x0 + 2 t4 + {0,1}]; B(x) = Σ_c q̃_c(x,l1) wr2_x T[c][x] is
+// accumulated per lane against the wr2-weighted l1 table and reduced across the warp once
+// per triple.  Per 8 columns: 9 DMMA + 18 DMUL/DFMA (S) + 2 DFMA + 17 loads.
+// ------------------------------------------------------------------------------------------
+template <int PP>
+__host__ __device__ constexpr int ns_groups() { return (PP / 2) * (PP / 4) + (PP / 2 + 3) / 4; }
+template <int PP>
+__host__ __device__ constexpr int ns_gd(int k) {
+    return k < (PP / 2) * (PP / 4) ? k / (PP / 4) : PP / 2;
+}
+template <int PP>
+__host__ __device__ constexpr int ns_gi0(int k) {
+    return k < (PP / 2) * (PP / 4) ? (k % (PP / 4)) * 4 : (k - (PP / 2) * (PP / 4)) * 4;
+}
+template <int PP>
+struct NsAfrag {
+    double a[ns_groups<PP>()][32];  // [k-step][lane]: lane (g, t4) holds Ã[g][pair(k, t4)]
+};
+
+// QT2[l][xb][c2][8] = q̃[c2 mod PP][8 xb + i][l] (0 for c2 mod PP >= p or x >= Nx);
+// Q1W[l][xb][c][8]  = wr2[x] q̃[c][x][l]; from the plan's QT[l][c][NxP].
+__global__ void k_ns_tables(const double* __restrict__ QT, const double* __restrict__ wr2, int p,
+                            int PP, int Nx, int NxP, int L, int XB8, double* __restrict__ QT2,
+                            double* __restrict__ Q1W) {
+    const int64_t total = (int64_t)L * XB8 * 2 * PP * 8;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int xi = (int)(i & 7);
+        int64_t r = i >> 3;
+        const int c2 = (int)(r % (2 * PP));
+        r /= 2 * PP;
+        const int xb = (int)(r % XB8);
+        const int l = (int)(r / XB8);
+        const int c = c2 % PP, x = xb * 8 + xi;
+        const double val = (c < p && x < Nx) ? QT[((int64_t)l * p + c) * NxP + x] : 0.0;
+        QT2[i] = val;
+        if (c2 < PP) Q1W[(((int64_t)l * XB8 + xb) * PP + c) * 8 + xi] = x < Nx ? wr2[x] * val : 0.0;
+    }
+}
+
+// WZ[t] = W_t zm_t of the resident sparse domain (once per domain).
+__global__ void k_ns_weights(const int4* __restrict__ trip, const double* __restrict__ W,
+                             int64_t count, const double* __restrict__ C,
+                             const double* __restrict__ v, const double* __restrict__ lf,
+                             int mode, int l_min, double* __restrict__ WZ) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 tr = trip[t];
+        WZ[t] = W[t] * zm_weight(mode, tr.x, tr.y, tr.z, C, v, l_min, lf);
+    }
+}
+
+#ifndef NSD_THREADS_
+#define NSD_THREADS_ 128
+#endif
+constexpr int NSD_THREADS = NSD_THREADS_;
+
+template <int PP>
+__global__ void __launch_bounds__(NSD_THREADS)
+k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int64_t count,
+              const double* __restrict__ QT2, const double* __restrict__ Q1W, int XB8,
+              const NsAfrag<PP> af, const double* __restrict__ q, const int* __restrict__ modes,
+              int P, int nm, int L, int l_min, double* __restrict__ partial) {
+    constexpr int NK = ns_groups<PP>();
+    constexpr int NW = NSD_THREADS / 32;
+    extern __shared__ double sh[];
+    double* bacc = sh;                                         // [NW][nm]
+    int* md = reinterpret_cast<int*>(bacc + (size_t)NW * nm);  // [nm][3]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    for (int i = tid; i < NW * nm; i += NSD_THREADS) bacc[i] = 0.0;
+    for (int i = tid; i < 3 * nm; i += NSD_THREADS) md[i] = modes[i];
+    double a[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) a[k] = af.a[k][lane];
+    __syncthreads();
+    double* my = bacc + (size_t)warp * nm;
+    const int64_t s2 = (int64_t)XB8 * 2 * PP * 8, s1 = (int64_t)XB8 * PP * 8;
+    const int64_t nwarps = (int64_t)gridDim.x * NW;
+    for (int64_t t = (int64_t)blockIdx.x * NW + warp; t < count; t += nwarps) {
+        const int4 tr = trip[t];
+        const double* p2 = QT2 + (tr.y - l_min) * s2 + t4 * 8 + g;
+        const double* p3 = QT2 + (tr.z - l_min) * s2 + t4 * 8 + g;
+        const double* p1 = Q1W + (tr.x - l_min) * s1 + g * 8 + 2 * t4;
+        double xs0 = 0.0, xs1 = 0.0;
+#pragma unroll 2
+        for (int xb = 0; xb < XB8; ++xb) {
+            double r2[PP], r3[PP];
+#pragma unroll
+            for (int i = 0; i < PP; ++i) {
+                r2[i] = __ldg(p2 + i * 8);
+                r3[i] = __ldg(p3 + i * 8);
+            }
+            const double2 w = __ldg(reinterpret_cast<const double2*>(p1));
+            double acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < NK; ++k) {
+                const int i0 = ns_gi0<PP>(k), j = (ns_gi0<PP>(k) + ns_gd<PP>(k)) % PP;
+                const double s = r2[i0] * r3[j] + r2[j] * r3[i0];
+                dmma884(acc, a[k], s);
+            }
+            xs0 = fma(w.x, acc[0], xs0);
+            xs1 = fma(w.y, acc[1], xs1);
+            p2 += 2 * PP * 8;
+            p3 += 2 * PP * 8;
+            p1 += PP * 8;
+        }
+        double xs = xs0 + xs1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+        ns_project(tr, WZ[t] * xs, q, md, P, nm, L, l_min, lane, my);
+    }
+    __syncthreads();
+    for (int m = tid; m < nm; m += NSD_THREADS) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += bacc[(size_t)w * nm + m];
+        partial[(int64_t)blockIdx.x * nm + m] = s;
+    }
+}
+
+// Ã fragments of the DMMA kernel from the symmetric table at[c][pair] (see above).
+template <int PP>
+static NsAfrag<PP> ns_afrag(const std::vector<double>& at, int p, int P2) {
+    NsAfrag<PP> f;
+    for (int k = 0; k < ns_groups<PP>(); ++k)
+        for (int lane = 0; lane < 32; ++lane) {
+            const int g = lane >> 2, t4 = lane & 3, d = ns_gd<PP>(k), r = ns_gi0<PP>(k) + t4;
+            const int a = r % PP, b = (r + d) % PP;
+            const bool ok = (2 * d < PP || r < PP / 2) && a < p && b < p && g < p;
+            f.a[k][lane] = ok ? at[(size_t)g * P2 + pair_idx(std::min(a, b), std::max(a, b))] : 0.0;
+        }
+    return f;
+}
+
+template <int PP>
+static void launch_nonsep_dmma(mg_plan* Pl, const std::vector<double>& at, cudaStream_t st) {
+    const int XB8 = ceil_div(Pl->Nx, 8);
+    if (!Pl->ns_qt2.p) {  // x-blocked, rotation-doubled q̃ tables (once per plan)
+        Pl->ns_qt2.alloc((size_t)Pl->L * XB8 * 2 * PP * 8);
+        Pl->ns_q1w.alloc((size_t)Pl->L * XB8 * PP * 8);
+        k_ns_tables<<<1184, 256, 0, st>>>(Pl->QT.p, Pl->wr2.p, Pl->p, PP, Pl->Nx, Pl->NxP, Pl->L,
+                                          XB8, Pl->ns_qt2.p, Pl->ns_q1w.p);
+        MG_LAUNCHED();
+    }
+    const NsAfrag<PP> af = ns_afrag<PP>(at, Pl->p, Pl->P2);
+    const size_t shm = (size_t)(NSD_THREADS / 32) * Pl->nm * 8 + (size_t)3 * Pl->nm * 4;
+    static int resident[64] = {0};
+    int& res = resident[Pl->device & 63];
+    if (!res) {
+        MG_CUDA(cudaFuncSetAttribute(k_nonsep_dmma<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     100 * 1024));
+        MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_nonsep_dmma<PP>, NSD_THREADS,
+                                                              shm));
+        res = std::max(res, 1);
+    }
+    int sms = 148;
+    MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, Pl->device));
+    Pl->ns_blocks = sms * res;
+    Pl->ns_part.ensure((size_t)Pl->ns_blocks * Pl->nm);
+    k_nonsep_dmma<PP><<<Pl->ns_blocks, NSD_THREADS, shm, st>>>(
+        reinterpret_cast<const int4*>(Pl->ns_trip.p), Pl->ns_wz.p, Pl->ns_count, Pl->ns_qt2.p,
+        Pl->ns_q1w.p, XB8, af, Pl->q.p, Pl->modes.p, Pl->p, Pl->nm, Pl->L, Pl->l_min,
+        Pl->ns_part.p);
+}
+
 template <int P>
 static void launch_nonsep_warp(mg_plan* Pl, const std::vector<double>& at, cudaStream_t st) {
     NsAlpha<P> al;
@@ -1621,6 +1802,11 @@ void nonsep_set_domain(mg_plan* P, const int32_t* l1, const int32_t* l2, const i
     if (!count) return;
     P->ns_trip.upload(packed.data(), packed.size());
     P->ns_W.upload(W, count);
+    P->ns_wz.ensure(count);
+    k_ns_weights<<<std::min<int64_t>((count + 255) / 256, 4096), 256>>>(
+        reinterpret_cast<const int4*>(P->ns_trip.p), P->ns_W.p, count, P->C.p, P->v.p, P->lf.p,
+        P->h2_mode, P->l_min, P->ns_wz.p);
+    MG_LAUNCHED();
     MG_CUDA(cudaStreamSynchronize(0));  // packed is pageable host memory
 }
 
@@ -1650,9 +1836,12 @@ void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_ho
         MG_REQUIRE((size_t)(NSW_THREADS / 32) * nm * 8 + (size_t)3 * nm * 4 <= 100 * 1024,
                    "too many modes for the non-separable kernel");
         ns_mark(P, st);  // (start, end) event pair, resolved lazily by nonsep_collect
-        switch (p) {
+        static const bool no_dmma = std::getenv("MG_NS_DFMA") != nullptr;  // A/B switch
+        switch ((no_dmma || p > 8) ? 100 + p : p) {
+            case 1: case 2: case 3: case 4: launch_nonsep_dmma<4>(P, at, st); break;
+            case 5: case 6: case 7: case 8: launch_nonsep_dmma<8>(P, at, st); break;
 #define MG_NS_CASE(N) \
-    case N: launch_nonsep_warp<N>(P, at, st); break;
+    case 100 + N: launch_nonsep_warp<N>(P, at, st); break;
             MG_NS_CASE(1) MG_NS_CASE(2) MG_NS_CASE(3) MG_NS_CASE(4) MG_NS_CASE(5) MG_NS_CASE(6)
             MG_NS_CASE(7) MG_NS_CASE(8) MG_NS_CASE(9) MG_NS_CASE(10) MG_NS_CASE(11)
             MG_NS_CASE(12) MG_NS_CASE(13) MG_NS_CASE(14) MG_NS_CASE(15) MG_NS_CASE(16)

@@ -98,8 +98,11 @@ struct mg_plan {
     // resident sparse domain + buffers of the non-separable path
     mg::DBuf<int32_t> ns_trip;  // [count][4] = l1, l2, l3, 0
     mg::DBuf<double> ns_W, ns_part, ns_b, ns_alpha;
+    mg::DBuf<double> ns_wz;          // [count] W_t * zm_t (h2_mode of the plan), DMMA kernel
+    mg::DBuf<double> ns_qt2, ns_q1w; // x-blocked q̃ tables of the DMMA kernel (built lazily)
     int64_t ns_count = 0;
     int ns_blocks = 0;
+    int ns_dmma_blocks = 0;
     std::vector<cudaEvent_t> ns_events;  // (start, end) pairs of profiled nonsep calls
     size_t ns_used = 0;
 };

@@ -143,3 +143,36 @@ class TestInputs:
         qt = qtilde_ref.qtilde(hi.k, hi.wk, hi.x, hi.qk, d, 2, 200, ells=[2, 77, 200])
         for l in (2, 77, 200):
             assert np.array_equal(qt[:, :, l - 2], g_c0["qt"][:, :, l - 2])
+
+
+class TestNonsepPin:
+    """The config-3 restatement (oracle/nonsep_ref.py) against the unmodified reference's own
+    per-triple functions — radial_integral_x, late_product_y, _triple_z,
+    permutation_multiplicity in gamma3d_naive's loop structure (engine3d.py:41-83,189-215) —
+    on 240 seeded config-3 triples incl. odd-parity and step-10 cells, both h2 modes
+    (tests/golden/make_c3_golden.py)."""
+
+    @pytest.mark.parametrize("mode", ["gosper", "exact"])
+    def test_sample_matches_reference_functions(self, mode):
+        from conftest import golden
+        from oracle import nonsep_ref
+        from paper_1503_08809_b200.configs import sparse_domain, sparse_grid
+        g = golden("c3.npz")
+        hi = host_inputs("c3")
+        l1, l2, l3, W = sparse_domain(*sparse_grid(l_max=hi.l_max))
+        assert l1.size == int(g["count"]) == 724930
+        qt = np.zeros((hi.spec.p, hi.x.size, hi.l_max - 1))
+        qt[:, :, g["grid"] - 2] = g["qt_grid"]
+        i = g["sample_idx"]
+        assert ((l1[i] + l2[i] + l3[i]) % 2 == 1).any() and (W[i] != 1.0).any()
+        b = nonsep_ref.nonsep(hi.q, qt, g["C"], hi.v, hi.wr2, hi.entries, hi.alpha, 2, l1[i],
+                              l2[i], l3[i], W[i], h2_mode=mode)
+        assert frob_rel(b, g[f"sample_b_{mode}"]) < 1e-13
+
+    def test_exact_mode_gates_odd_parity(self):
+        """h2_exact is exactly 0 off the triangle / even-parity set (geometry.py:67-71)."""
+        l1 = np.array([2, 3, 2, 10])
+        l2 = np.array([2, 3, 3, 10])
+        l3 = np.array([2, 3, 4, 25])          # even ok, odd sum, odd sum, no triangle
+        h = ref.h2_exact(l1, l2, l3)
+        assert h[0] > 0 and h[1] == 0 and h[2] == 0 and h[3] == 0
