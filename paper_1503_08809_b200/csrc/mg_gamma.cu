@@ -1567,14 +1567,13 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int nblocks, 
 // pair (a, b) that depends on t4.  The K order makes those register indices compile-time:
 // the 36 unordered pairs of Z_PP are grouped by cyclic difference d = b - a (mod PP) into
 // groups of 4 consecutive rotations {(r, r+d) : r = i0..i0+3}, and lane t4 holds its q̃
-// components ROTATED by t4 (register i = component (i + t4) mod PP, read from a table whose
-// component axis is stored twice so that i + t4 never wraps).  Pair (i0 + t4, i0 + d + t4)
+// components ROTATED by t4 (register i = component (i + t4) mod PP: per-lane offsets).  Pair (i0 + t4, i0 + d + t4)
 // is then registers (i0, (i0 + d) mod PP) in every lane: 9 k-steps at PP = 8, no padding.
 //   rotations r < PP/2 only for d = PP/2 (r and r + PP/2 are the same pair);
 //   p < PP: components >= p are zero in the tables and the Ã fragments.
 // C fragment: lane holds T[c = g][x0 + 2 t4 + {0,1}]; B(x) = Σ_c q̃_c(x,l1) wr2_x T[c][x] is
 // accumulated per lane against the wr2-weighted l1 table and reduced across the warp once
-// per triple.  Per 8 columns: 9 DMMA + 18 DMUL/DFMA (S) + 2 DFMA + 17 loads.
+// per triple.  Per 8 columns: 9 DMMA + 18 DMUL/DFMA (S) + 2 DFMA + 17 shared-memory loads.
 // ------------------------------------------------------------------------------------------
 template <int PP>
 __host__ __device__ constexpr int ns_groups() { return (PP / 2) * (PP / 4) + (PP / 2 + 3) / 4; }
@@ -1591,24 +1590,30 @@ struct NsAfrag {
     double a[ns_groups<PP>()][32];  // [k-step][lane]: lane (g, t4) holds Ã[g][pair(k, t4)]
 };
 
-// QT2[l][xb][c2][8] = q̃[c2 mod PP][8 xb + i][l] (0 for c2 mod PP >= p or x >= Nx);
-// Q1W[l][xb][c][8]  = wr2[x] q̃[c][x][l]; from the plan's QT[l][c][NxP].
+// Tables of the DMMA kernel, x in blocks of 8 columns ("chunks"), one 8-column row per
+// component, PP*64 bytes per (l, chunk):
+//   QTS[l][xb][c][8]: q̃[c][8 xb + i][l] at column position (i + 4 ((c >> 1) & 1)) & 7 —
+//                     the swizzle makes the rotated B-operand reads bank-conflict free (a half
+//                     warp reads 4 consecutive components x 4 columns: the two component pairs
+//                     land on opposite column halves of the 128-byte bank window);
+//   Q1W[l][xb][c][8]: wr2[x] q̃[c][x][l] (no swizzle: read as double2 per lane).
+// Components >= p and columns >= Nx are zero.  Built from the plan's QT[l][c][NxP].
 __global__ void k_ns_tables(const double* __restrict__ QT, const double* __restrict__ wr2, int p,
-                            int PP, int Nx, int NxP, int L, int XB8, double* __restrict__ QT2,
+                            int PP, int Nx, int NxP, int L, int XB8, double* __restrict__ QTS,
                             double* __restrict__ Q1W) {
-    const int64_t total = (int64_t)L * XB8 * 2 * PP * 8;
+    const int64_t total = (int64_t)L * XB8 * PP * 8;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int xi = (int)(i & 7);
         int64_t r = i >> 3;
-        const int c2 = (int)(r % (2 * PP));
-        r /= 2 * PP;
+        const int c = (int)(r % PP);
+        r /= PP;
         const int xb = (int)(r % XB8);
         const int l = (int)(r / XB8);
-        const int c = c2 % PP, x = xb * 8 + xi;
+        const int x = xb * 8 + xi;
         const double val = (c < p && x < Nx) ? QT[((int64_t)l * p + c) * NxP + x] : 0.0;
-        QT2[i] = val;
-        if (c2 < PP) Q1W[(((int64_t)l * XB8 + xb) * PP + c) * 8 + xi] = x < Nx ? wr2[x] * val : 0.0;
+        Q1W[i] = x < Nx ? wr2[x] * val : 0.0;
+        QTS[(i & ~(int64_t)7) + ((xi + 4 * ((c >> 1) & 1)) & 7)] = val;
     }
 }
 
@@ -1624,60 +1629,164 @@ __global__ void k_ns_weights(const int4* __restrict__ trip, const double* __rest
     }
 }
 
+// Staging of the B-operand inputs.  Read straight from global memory, the rotated layout
+// costs 16 LDG.64 per lane per chunk (every component is read by all four lanes of a quad)
+// and round 2's first version was bound by L1 wavefronts (one 256-byte LDG.64 occupies the
+// L1 data pipe for ~4 cycles; profiles/r02_ncu_nonsep_dmma_v1.txt).  Here each warp streams
+// its triples' data into shared memory with cp.async.bulk (TMA engine, no LSU wavefronts),
+// NS_ST stages of NS_CH chunks: [l2 chunks][l3 chunks], completing on a per-warp, per-stage
+// mbarrier; the rotated reads are then LDS.64 (2 wavefronts each).  The wr2-weighted l1 row
+// (one double2 per lane per chunk, no redundancy) is read from global memory.  12 warps per
+// CTA (3 per SM sub-partition) with NS_CH = 4 accumulator chains each: a single chain is
+// latency-bound, the sub-partition's DMMA pipe needs several in flight.
+// Lane 0 of the warp is the producer: after the warp has consumed a stage it refills the slot
+// with the stage NS_ST ahead (crossing into the warp's next triple), so copies run under the
+// DMMAs of the stages in between.
 #ifndef NSD_THREADS_
-#define NSD_THREADS_ 128
+#define NSD_THREADS_ 384
 #endif
 constexpr int NSD_THREADS = NSD_THREADS_;
+#ifndef NS_CH
+#define NS_CH 4  // chunks of 8 x columns per stage
+#endif
+#ifndef NS_ST
+#define NS_ST 3  // stages per warp
+#endif
 
 template <int PP>
-__global__ void __launch_bounds__(NSD_THREADS)
+struct NsStage {
+    static constexpr int CHUNK = PP * 8;                 // doubles per (l, chunk)
+    static constexpr int DOUBLES = 2 * NS_CH * CHUNK;     // l2, l3 blocks
+    static constexpr size_t WARP_BYTES = (size_t)NS_ST * DOUBLES * 8 + NS_ST * 8;
+};
+
+template <int PP>
+__global__ void __launch_bounds__(NSD_THREADS, 1)
 k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int64_t count,
-              const double* __restrict__ QT2, const double* __restrict__ Q1W, int XB8,
+              const double* __restrict__ QTS, const double* __restrict__ Q1W, int XB8,
               const NsAfrag<PP> af, const double* __restrict__ q, const int* __restrict__ modes,
               int P, int nm, int L, int l_min, double* __restrict__ partial) {
-    constexpr int NK = ns_groups<PP>();
+    using SG = NsStage<PP>;
+    constexpr int NK = ns_groups<PP>(), CH = NS_CH, NST = NS_ST, CHUNK = SG::CHUNK;
     constexpr int NW = NSD_THREADS / 32;
-    extern __shared__ double sh[];
-    double* bacc = sh;                                         // [NW][nm]
-    int* md = reinterpret_cast<int*>(bacc + (size_t)NW * nm);  // [nm][3]
+    extern __shared__ __align__(16) double sh[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t4 = lane & 3;
+    // [NW warps x NST stages x DOUBLES][NW x NST mbarriers][NW][nm] partial b [3 nm] modes
+    double* stg = sh + (size_t)warp * NST * SG::DOUBLES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sh + (size_t)NW * NST * SG::DOUBLES) + warp * NST;
+    double* bacc = reinterpret_cast<double*>(reinterpret_cast<uint64_t*>(
+                       sh + (size_t)NW * NST * SG::DOUBLES) + NW * NST);
+    int* md = reinterpret_cast<int*>(bacc + (size_t)NW * nm);
     for (int i = tid; i < NW * nm; i += NSD_THREADS) bacc[i] = 0.0;
     for (int i = tid; i < 3 * nm; i += NSD_THREADS) md[i] = modes[i];
+    if (lane == 0) {
+        for (int s = 0; s < NST; ++s) mbar_init(full + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
     double a[NK];
 #pragma unroll
     for (int k = 0; k < NK; ++k) a[k] = af.a[k][lane];
+    // lane's rotated component offsets (doubles) within a chunk block: register i holds
+    // component (i + t4) mod PP of column g, stored at swizzled column position
+    int off[PP];
+#pragma unroll
+    for (int i = 0; i < PP; ++i) {
+        const int c = (i + t4) % PP;
+        off[i] = c * 8 + ((g + 4 * ((c >> 1) & 1)) & 7);
+    }
     __syncthreads();
     double* my = bacc + (size_t)warp * nm;
-    const int64_t s2 = (int64_t)XB8 * 2 * PP * 8, s1 = (int64_t)XB8 * PP * 8;
     const int64_t nwarps = (int64_t)gridDim.x * NW;
+    const int nstg = (XB8 + CH - 1) / CH;  // stages per triple
+    const int64_t lstride = (int64_t)XB8 * CHUNK;
+
+    // producer cursor (lane 0): the (triple, stage) to issue next
+    int64_t pt = (int64_t)blockIdx.x * NW + warp;
+    int ps = 0;
+    int4 ptr = pt < count ? trip[pt] : make_int4(0, 0, 0, 0);
+    auto issue = [&](int slot) {
+        if (pt >= count) return;
+        const int c0 = ps * CH, nch = min(CH, XB8 - c0);
+        const uint32_t bytes = (uint32_t)nch * CHUNK * 8;
+        double* st = stg + (size_t)slot * SG::DOUBLES;
+        mbar_arrive_expect_tx(full + slot, 2 * bytes);
+        bulk_g2s(st, QTS + (ptr.y - l_min) * lstride + (int64_t)c0 * CHUNK, bytes, full + slot);
+        bulk_g2s(st + CH * CHUNK, QTS + (ptr.z - l_min) * lstride + (int64_t)c0 * CHUNK, bytes,
+                 full + slot);
+        if (++ps == nstg) {
+            ps = 0;
+            pt += nwarps;
+            if (pt < count) ptr = trip[pt];
+        }
+    };
+    if (lane == 0)
+        for (int s = 0; s < NST; ++s) issue(s);
+    __syncwarp();
+
+    uint32_t gst = 0;  // stages consumed by this warp (slot = gst % NST, phase = gst / NST)
     for (int64_t t = (int64_t)blockIdx.x * NW + warp; t < count; t += nwarps) {
         const int4 tr = trip[t];
-        const double* p2 = QT2 + (tr.y - l_min) * s2 + t4 * 8 + g;
-        const double* p3 = QT2 + (tr.z - l_min) * s2 + t4 * 8 + g;
-        const double* p1 = Q1W + (tr.x - l_min) * s1 + g * 8 + 2 * t4;
+        const double* p1 = Q1W + (tr.x - l_min) * lstride + g * 8 + 2 * t4;
         double xs0 = 0.0, xs1 = 0.0;
-#pragma unroll 2
-        for (int xb = 0; xb < XB8; ++xb) {
-            double r2[PP], r3[PP];
+        for (int s = 0; s < nstg; ++s, ++gst) {
+            const int slot = (int)(gst % NST);
+            mbar_wait(full + slot, (int)((gst / NST) & 1));
+            const double* st = stg + (size_t)slot * SG::DOUBLES;
+            const int nch = min(CH, XB8 - s * CH);
 #pragma unroll
-            for (int i = 0; i < PP; ++i) {
-                r2[i] = __ldg(p2 + i * 8);
-                r3[i] = __ldg(p3 + i * 8);
-            }
-            const double2 w = __ldg(reinterpret_cast<const double2*>(p1));
-            double acc[2] = {0.0, 0.0};
+            // All NS_CH chunks of the stage at once: their pair products S first (each chunk's
+            // rotated q̃ rows are dead once its 9 S values exist), then the DMMAs of the
+            // NS_CH independent accumulator chains interleaved k-step by k-step, so a warp
+            // keeps NS_CH DMMAs in flight (the DMMA D -> C latency is ~4 issue slots of the
+            // sub-partition's DMMA pipe).
+            double S[CH][NK];
 #pragma unroll
-            for (int k = 0; k < NK; ++k) {
-                const int i0 = ns_gi0<PP>(k), j = (ns_gi0<PP>(k) + ns_gd<PP>(k)) % PP;
-                const double s = r2[i0] * r3[j] + r2[j] * r3[i0];
-                dmma884(acc, a[k], s);
+            for (int u = 0; u < CH; ++u) {
+                if (u < nch) {
+                    const double* b2 = st + u * CHUNK;
+                    const double* b3 = st + (CH + u) * CHUNK;
+                    double r2[PP], r3[PP];
+#pragma unroll
+                    for (int i = 0; i < PP; ++i) {
+                        r2[i] = b2[off[i]];
+                        r3[i] = b3[off[i]];
+                    }
+#pragma unroll
+                    for (int k = 0; k < NK; ++k) {
+                        const int i0 = ns_gi0<PP>(k), j = (ns_gi0<PP>(k) + ns_gd<PP>(k)) % PP;
+                        S[u][k] = r2[i0] * r3[j] + r2[j] * r3[i0];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NK; ++k) S[u][k] = 0.0;
+                }
             }
-            xs0 = fma(w.x, acc[0], xs0);
-            xs1 = fma(w.y, acc[1], xs1);
-            p2 += 2 * PP * 8;
-            p3 += 2 * PP * 8;
-            p1 += PP * 8;
+            double acc[CH][2];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) acc[u][0] = acc[u][1] = 0.0;
+#pragma unroll
+            for (int k = 0; k < NK; ++k)
+#pragma unroll
+                for (int u = 0; u < CH; ++u) dmma884(acc[u], a[k], S[u][k]);
+            // accumulator row c = g exists only for g < PP (PP = 4: lanes g >= 4 hold zero
+            // rows of T and must not read past their chunk's PP component rows)
+            const double* b1 = p1 + (int64_t)s * CH * CHUNK;
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const double2 w = (u < nch && g < PP)
+                                      ? __ldg(reinterpret_cast<const double2*>(b1 + u * CHUNK))
+                                      : make_double2(0.0, 0.0);
+                xs0 = fma(w.x, acc[u][0], xs0);
+                xs1 = fma(w.y, acc[u][1], xs1);
+            }
+            // slot consumed by every lane: refill it with the stage NST ahead
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                issue(slot);
+            }
+            __syncwarp();
         }
         double xs = xs0 + xs1;
 #pragma unroll
@@ -1709,27 +1818,27 @@ static NsAfrag<PP> ns_afrag(const std::vector<double>& at, int p, int P2) {
 template <int PP>
 static void launch_nonsep_dmma(mg_plan* Pl, const std::vector<double>& at, cudaStream_t st) {
     const int XB8 = ceil_div(Pl->Nx, 8);
-    if (!Pl->ns_qt2.p) {  // x-blocked, rotation-doubled q̃ tables (once per plan)
-        Pl->ns_qt2.alloc((size_t)Pl->L * XB8 * 2 * PP * 8);
+    if (!Pl->ns_qt2.p) {  // x-chunked, swizzled q̃ tables (once per plan)
+        Pl->ns_qt2.alloc((size_t)Pl->L * XB8 * PP * 8);
         Pl->ns_q1w.alloc((size_t)Pl->L * XB8 * PP * 8);
         k_ns_tables<<<1184, 256, 0, st>>>(Pl->QT.p, Pl->wr2.p, Pl->p, PP, Pl->Nx, Pl->NxP, Pl->L,
                                           XB8, Pl->ns_qt2.p, Pl->ns_q1w.p);
         MG_LAUNCHED();
     }
     const NsAfrag<PP> af = ns_afrag<PP>(at, Pl->p, Pl->P2);
-    const size_t shm = (size_t)(NSD_THREADS / 32) * Pl->nm * 8 + (size_t)3 * Pl->nm * 4;
-    static int resident[64] = {0};
-    int& res = resident[Pl->device & 63];
-    if (!res) {
+    constexpr int NW = NSD_THREADS / 32;
+    const size_t shm = NW * NsStage<PP>::WARP_BYTES + (size_t)NW * Pl->nm * 8 +
+                       (size_t)3 * Pl->nm * 4;
+    MG_REQUIRE(shm <= 227 * 1024, "too many modes for the non-separable DMMA kernel");
+    static bool attr[64] = {false};
+    if (!attr[Pl->device & 63]) {
         MG_CUDA(cudaFuncSetAttribute(k_nonsep_dmma<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     100 * 1024));
-        MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_nonsep_dmma<PP>, NSD_THREADS,
-                                                              shm));
-        res = std::max(res, 1);
+                                     227 * 1024));
+        attr[Pl->device & 63] = true;
     }
     int sms = 148;
     MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, Pl->device));
-    Pl->ns_blocks = sms * res;
+    Pl->ns_blocks = sms;  // one CTA of NW warps per SM (shared memory holds every warp's stages)
     Pl->ns_part.ensure((size_t)Pl->ns_blocks * Pl->nm);
     k_nonsep_dmma<PP><<<Pl->ns_blocks, NSD_THREADS, shm, st>>>(
         reinterpret_cast<const int4*>(Pl->ns_trip.p), Pl->ns_wz.p, Pl->ns_count, Pl->ns_qt2.p,

@@ -199,3 +199,34 @@ def test_device_selection(monkeypatch):
     assert resolve_devices() == [0]                          # no GPU here: one (failing) device
     with pytest.raises(ValueError):
         resolve_devices(None, [])
+
+
+def test_integration_shim_rebinds_reference_names():
+    """paper_1503_08809_b200.integration.install rebinds exactly the reference's engine
+    names (cmbproj, engine3d, harness; harness.py:19-21) and uninstall restores them."""
+    import sys
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "cmbproj")):
+            if path not in sys.path:
+                sys.path.append(path)
+            break
+    cp = pytest.importorskip("cmbproj")
+    from paper_1503_08809_b200 import integration
+    before = (cp.gamma3d_matrix, cp.engine3d.gamma3d_matrix, cp.harness.gamma3d_matrix,
+              cp.gamma2d_matrix, cp.engine2d.gamma2d_matrix, cp.harness.gamma2d_matrix)
+    saved = integration.install(cp)
+    try:
+        for fn in (cp.gamma3d_matrix, cp.engine3d.gamma3d_matrix, cp.harness.gamma3d_matrix,
+                   cp.gamma2d_matrix, cp.engine2d.gamma2d_matrix, cp.harness.gamma2d_matrix):
+            assert getattr(fn, "__wrapped_b200__", False)
+        assert cp.gamma3d_naive is not None and not hasattr(cp.gamma3d_naive, "__wrapped_b200__")
+        import inspect
+        ref_sig = inspect.signature(before[1])
+        assert list(inspect.signature(cp.gamma3d_matrix).parameters) == list(ref_sig.parameters)
+        assert list(inspect.signature(cp.gamma2d_matrix).parameters) == \
+            list(inspect.signature(before[4]).parameters)
+    finally:
+        integration.uninstall(saved)
+    after = (cp.gamma3d_matrix, cp.engine3d.gamma3d_matrix, cp.harness.gamma3d_matrix,
+             cp.gamma2d_matrix, cp.engine2d.gamma2d_matrix, cp.harness.gamma2d_matrix)
+    assert all(a is b for a, b in zip(before, after))
