@@ -46,6 +46,12 @@ const char* mg_last_error(void);
 /* Number of visible CUDA devices (0 without a GPU; never fails). */
 int mg_device_count(void);
 
+/* Bounds-check counters of a CHECKED build (compiled with -DMG_CHECKED=1; compute-sanitizer is
+ * not available on this pool): counts[i] = number of out-of-extent global writes / bulk-copy
+ * source ranges seen at check site i (n <= 16 sites, see MgCheck in mg_gamma.cu) on `device`
+ * since the last reset; *checked = 1 for a checked build, 0 otherwise (counts all zero). */
+int mg_debug_checks(uint32_t* counts, int n, int reset, int* checked, int device);
+
 /* ---------------------------------------------------------------------------------------
  * Domain: replaces TriangularDomain / enumerate_domain (geometry.py:145-200).
  * Ordered triples l1<=l2<=l3<=l_max, l3<=l1+l2, l1+l2+l3 even, lexicographic order

@@ -29,6 +29,7 @@ _SIGS = {
     "mg_version": (_i, []),
     "mg_last_error": (ctypes.c_char_p, []),
     "mg_device_count": (_i, []),
+    "mg_debug_checks": (_i, [_vp, _i, _i, _vp, _i]),
     "mg_domain_count": (_i, [_i, _i, _vp, _vp]),
     "mg_domain_triples": (_i, [_i, _i, _i64, _i64, _vp, _vp, _vp, _i]),
     "mg_domain_match_range": (_i, [_i, _i, _vp, _vp, _vp, _i64, _vp]),
@@ -98,6 +99,20 @@ def check(rc: int) -> None:
     if rc == 2:
         raise MemoryError(msg)
     raise NativeError(msg)
+
+
+CHECK_SITES = ("panel write", "K1 panel source", "K1 WQB source", "K1 H write",
+               "pair-product S write", "K2 S source", "K2 H source", "K2 G write",
+               "gather R/Sq write", "K3 Sq source", "K3 R source", "K3 Z write",
+               "non-separable QTS source", "non-separable Q1W read", "non-separable triple l-range")
+
+
+def debug_checks(reset: bool = False, device: int = 0):
+    """(checked_build, {site: violations}) from a library built with -DMG_CHECKED=1."""
+    counts = np.zeros(16, np.uint32)
+    flag = np.zeros(1, np.int32)
+    check(lib().mg_debug_checks(ptr(counts), 16, int(reset), ptr(flag), int(device)))
+    return bool(flag[0]), {s: int(c) for s, c in zip(CHECK_SITES, counts)}
 
 
 def ptr(a: np.ndarray | None):

@@ -158,6 +158,15 @@ int mg_version(void) { return 100; }
 
 const char* mg_last_error(void) { return g_last_error.c_str(); }
 
+int mg_debug_checks(uint32_t* counts, int n, int reset, int* checked, int device) {
+    return guarded([&] {
+        MG_REQUIRE(counts && n >= 0, "invalid argument");
+        DeviceGuard g(device);
+        const int c = debug_checks(counts, n, reset != 0);
+        if (checked) *checked = c;
+    });
+}
+
 int mg_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {

@@ -35,6 +35,37 @@ namespace mg {
 #ifndef MG_RUN_WARPS
 #define MG_RUN_WARPS 12  // consumer warps of the 128 x 96 run/pair tile: 12 (32x32 per warp) or 16
 #endif
+// Checked build (MG_CHECKED=1: tools/build_variant.sh checked -DMG_CHECKED=1).  compute-
+// sanitizer is closed on this pool, so the pipeline kernels carry their own bounds checks:
+// every global-memory write and every bulk-copy (TMA) source range is checked against the
+// extent of its buffer, and violations are COUNTED per check site (no trap, no fault),
+// read back through mg_debug_checks().  In the normal build the checks compile to nothing.
+#ifndef MG_CHECKED
+#define MG_CHECKED 0
+#endif
+struct MgBounds {  // buffer extents in doubles (0 = unchecked)
+    int64_t panel, wqb, h, s, g, r, sq, z, qts, q1w;
+};
+enum MgCheck {
+    CK_PANEL_W, CK_K1_PANEL, CK_K1_WQB, CK_K1_H_W, CK_S_W, CK_K2_S, CK_K2_H, CK_K2_G_W,
+    CK_GATHER_W, CK_K3_SQ, CK_K3_R, CK_K3_Z_W, CK_NS_QTS, CK_NS_Q1W, CK_NS_L, CK_COUNT
+};
+#if MG_CHECKED
+static __device__ unsigned int g_chk[16];
+#define MG_DCHECK(cond, site)                                  \
+    do {                                                       \
+        if (!(cond)) atomicAdd(&g_chk[(int)(site)], 1u);       \
+    } while (0)
+#else
+#define MG_DCHECK(cond, site) \
+    do {                      \
+    } while (0)
+#endif
+// [lo, lo + n) inside [0, extent)
+__device__ __forceinline__ bool in_range(int64_t lo, int64_t n, int64_t extent) {
+    return lo >= 0 && n >= 0 && lo + n <= extent;
+}
+
 constexpr int RUN_TN = 96;              // run-contraction N tile ((c', x) columns)
 constexpr int RUN_TM_ = 128;            // (row, c) slots per tile
 constexpr int RUN_LDB = RUN_TN + 4;     // smem-identical row stride of WQB rows
@@ -138,7 +169,7 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
              const double* __restrict__ q, int L, int l_min, int p,
              const double* __restrict__ C, const double* __restrict__ v,
              const double* __restrict__ lf, const double* __restrict__ fl, int mode,
-             double* __restrict__ panel, unsigned magic_p) {
+             double* __restrict__ panel, unsigned magic_p, MgBounds bd) {
     extern __shared__ double zs[];  // [nrows][PANEL_JC]: zm of (row, j) for this chunk
     const MgTile tl = tiles[blockIdx.x];
     const int kt = (tl.jhi - tl.jlo + RUN_BK) / RUN_BK * RUN_BK;
@@ -179,6 +210,8 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
                     val = z * q[(int64_t)c * L + (l1 - l_min)];
                 }
             }
+            MG_DCHECK(in_range(poff[blockIdx.x] + (int64_t)(jc + jl) * RUN_LDA + slot, 1, bd.panel),
+                      CK_PANEL_W);
             out[(int64_t)(jc + jl) * RUN_LDA + slot] = val;
         }
         __syncthreads();
@@ -194,6 +227,7 @@ k_run_panels(const MgTile* __restrict__ tiles, const MgRow* __restrict__ rows,
 // CTAs (one per SM).  The producer warp streams the next item while consumers write H.
 struct RunItems {
     static constexpr bool kComputeA = false;
+    MgBounds bd;
     const MgTile* tiles;
     const int64_t* poff;
     const double* panel;
@@ -225,14 +259,17 @@ struct RunItems {
         const int ti = it / NB, nb = it - ti * NB;
         const MgTile& t = tiles[ti];
         if (lane == 0) {
+            MG_DCHECK(in_range(poff[ti] + (int64_t)kt * RUN_BK * RUN_LDA, RUN_BK * RUN_LDA, bd.panel),
+                      CK_K1_PANEL);
             bulk_g2s(As, panel + poff[ti] + (int64_t)kt * RUN_BK * RUN_LDA,
                      RUN_BK * RUN_LDA * sizeof(double), bar);
         } else {
             const int par = rows[t.row0].par;
-            const double* w = WQB + (par ? wbase.y : wbase.x) +
-                              ((int64_t)nb * (par ? wrows.y : wrows.x) + t.jlo + kt * RUN_BK) *
-                                  RUN_LDB;
-            bulk_g2s(Bs, w, RUN_BK * RUN_LDB * sizeof(double), bar);
+            const int64_t wo = (par ? wbase.y : wbase.x) +
+                               ((int64_t)nb * (par ? wrows.y : wrows.x) + t.jlo + kt * RUN_BK) *
+                                   RUN_LDB;
+            MG_DCHECK(in_range(wo, RUN_BK * RUN_LDB, bd.wqb), CK_K1_WQB);
+            bulk_g2s(Bs, WQB + wo, RUN_BK * RUN_LDB * sizeof(double), bar);
         }
     }
 };
@@ -243,11 +280,11 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
                const double* __restrict__ panel, int row_base, const MgRow* __restrict__ rows,
                const double* __restrict__ WQB, int p, int Nx, int Nxw, int NxP,
                longlong2 wbase, int2 wrows, double* __restrict__ H, unsigned magic_p,
-               unsigned magic_nx) {
+               unsigned magic_nx, MgBounds bd) {
     extern __shared__ __align__(16) double smem[];
     const int64_t ldb = (int64_t)p * Nxw;
-    RunItems items{tiles, poff, panel, rows, WQB, wbase, wrows, (int)((ldb + RUN_TN - 1) / RUN_TN),
-                   (int)ldb};
+    RunItems items{bd, tiles, poff, panel, rows, WQB, wbase, wrows,
+                   (int)((ldb + RUN_TN - 1) / RUN_TN), (int)ldb};
     const int nitems = ntiles * items.NB;
     const int64_t pp = (int64_t)p * p;
     const int XB = NxP / X_BK;
@@ -282,6 +319,7 @@ k_run_contract(const MgTile* __restrict__ tiles, int ntiles, const int64_t* __re
             for (int fm = 0; fm < CfgRun::FM; ++fm) {
                 if (!rok[fm] || MG_NO_EPI) continue;
                 double* h = H + roff[fm] + coff;
+                MG_DCHECK(!one || in_range(roff[fm] + coff, both ? 2 : 1, bd.h), CK_K1_H_W);
                 if (both) {
                     *reinterpret_cast<double2*>(h) =
                         make_double2(acc.c[fm][fn][0], acc.c[fm][fn][1]);
@@ -331,7 +369,7 @@ constexpr int PP_CHUNK = 16;  // pairs per block of the pair-product kernel
 // capping the run contraction at 120 registers to make room was measured slower).
 __global__ void __maxnreg__(MG_PP_MAXREG)
 k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __restrict__ QT,
-                int p, int P2, int NxP, int l_min, double* __restrict__ S) {
+                int p, int P2, int NxP, int l_min, double* __restrict__ S, MgBounds bd) {
     const int r = blockIdx.y;
     const MgRow rw = rows[row_b1 + r];
     const double2* q2 = reinterpret_cast<const double2*>(QT + (int64_t)(rw.l2 - l_min) * p * NxP);
@@ -357,12 +395,17 @@ k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __rest
                     w[k] = __ldg(q3 + (a + i + k) * nx2 + x);
                 }
 #pragma unroll
+                for (int k = 0; k < MG_PP_UNROLL; ++k) {
+                    MG_DCHECK(in_range(o + (int64_t)(pr + i + k) * X_LDK - S, 2, bd.s), CK_S_W);
+                }
+#pragma unroll
                 for (int k = 0; k < MG_PP_UNROLL; ++k)
                     *reinterpret_cast<double2*>(o + (int64_t)(pr + i + k) * X_LDK) =
                         make_double2(u[k].x * wb.x + ub.x * w[k].x, u[k].y * wb.y + ub.y * w[k].y);
             }
             for (; i < na; ++i) {
                 const double2 u = __ldg(q2 + (a + i) * nx2 + x), w = __ldg(q3 + (a + i) * nx2 + x);
+                MG_DCHECK(in_range(o + (int64_t)(pr + i) * X_LDK - S, 2, bd.s), CK_S_W);
                 *reinterpret_cast<double2*>(o + (int64_t)(pr + i) * X_LDK) =
                     make_double2(u.x * wb.x + ub.x * w.x, u.y * wb.y + ub.y * w.y);
             }
@@ -377,6 +420,7 @@ k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __rest
 template <class Cfg>
 struct XItems {
     static constexpr bool kComputeA = false;
+    MgBounds bd;
     const double* S;
     const double* H;
     int P2, pp, XB, MT, NT, kv_last;
@@ -406,12 +450,14 @@ struct XItems {
         decode(it, r, mt, nt);
         if (lane == 0) {
             const int mv = min(Cfg::BM, P2 - mt * Cfg::BM);
-            bulk_g2s(As, S + (((int64_t)r * XB + kt) * P2 + mt * Cfg::BM) * X_LDK,
-                     mv * X_LDK * sizeof(double), bar);
+            const int64_t so = (((int64_t)r * XB + kt) * P2 + mt * Cfg::BM) * X_LDK;
+            MG_DCHECK(in_range(so, (int64_t)mv * X_LDK, bd.s), CK_K2_S);
+            bulk_g2s(As, S + so, mv * X_LDK * sizeof(double), bar);
         } else {
             const int nv = min(Cfg::BN, pp - nt * Cfg::BN);
-            bulk_g2s(Bs, H + (((int64_t)r * XB + kt) * pp + nt * Cfg::BN) * X_LDK,
-                     nv * X_LDK * sizeof(double), bar);
+            const int64_t ho = (((int64_t)r * XB + kt) * pp + nt * Cfg::BN) * X_LDK;
+            MG_DCHECK(in_range(ho, (int64_t)nv * X_LDK, bd.h), CK_K2_H);
+            bulk_g2s(Bs, H + ho, nv * X_LDK * sizeof(double), bar);
         }
     }
 };
@@ -421,10 +467,11 @@ using XPipeP = PipeTMAPersistent<Cfg, X_BK, 3, false, false>;
 template <class Cfg>
 __global__ void __launch_bounds__(XPipeP<Cfg>::THREADS, 1)
 k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int nrows,
-               int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* __restrict__ G) {
+               int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* __restrict__ G,
+               MgBounds bd) {
     extern __shared__ __align__(16) double smem[];
     const int pp = p * p;
-    XItems<Cfg> items{S, H, P2, pp, NxP / X_BK, (P2 + Cfg::BM - 1) / Cfg::BM,
+    XItems<Cfg> items{bd, S, H, P2, pp, NxP / X_BK, (P2 + Cfg::BM - 1) / Cfg::BM,
                       (pp + Cfg::BN - 1) / Cfg::BN, 0};
     items.kv_last = Nx - (items.XB - 1) * X_BK;
     const int nitems = nrows * items.MT * items.NT;
@@ -436,6 +483,9 @@ k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int n
         acc_foreach_pair<Cfg>(acc, [&](int m, int n, double v0, double v1) {
             const int prr = m0 + m, cc = n0 + n;
             if (prr < P2 && !MG_NO_EPI) {
+                MG_DCHECK(cc >= pp || in_range(Gr + (int64_t)cc * P2 + prr - G, 1, bd.g), CK_K2_G_W);
+                MG_DCHECK(cc + 1 >= pp || in_range(Gr + (int64_t)(cc + 1) * P2 + prr - G, 1, bd.g),
+                          CK_K2_G_W);
                 if (cc < pp) Gr[(int64_t)cc * P2 + prr] = v0;
                 if (cc + 1 < pp) Gr[(int64_t)(cc + 1) * P2 + prr] = v1;
             }
@@ -487,9 +537,10 @@ static XTile choose_xtile(int P2, int pp) {
 
 template <class Cfg>
 static void launch_x(int num_sms, cudaStream_t st, const double* S, const double* H, int nrows,
-                     int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* G) {
+                     int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* G,
+                     const MgBounds& bd) {
     k_x_contract_p<Cfg><<<num_sms, XPipeP<Cfg>::THREADS, XPipeP<Cfg>::smem_bytes, st>>>(
-        S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G);
+        S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd);
 }
 template <class Cfg>
 static void attr_x() {
@@ -498,13 +549,13 @@ static void attr_x() {
 }
 static void launch_xtile(XTile xt, int num_sms, cudaStream_t st, const double* S, const double* H,
                          int nrows, int row_b1, int row_b3, int p, int P2, int Nx, int NxP,
-                         double* G) {
+                         double* G, const MgBounds& bd) {
     switch (xt) {
-        case XTile::T120: launch_x<CfgX120>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
-        case XTile::T120x96: launch_x<CfgX120x96>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
-        case XTile::T128x72: launch_x<CfgX128x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
-        case XTile::T160x72: launch_x<CfgX160x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
-        default: launch_x<CfgX128>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G); break;
+        case XTile::T120: launch_x<CfgX120>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
+        case XTile::T120x96: launch_x<CfgX120x96>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
+        case XTile::T128x72: launch_x<CfgX128x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
+        case XTile::T160x72: launch_x<CfgX160x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
+        default: launch_x<CfgX128>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
     }
 }
 
@@ -515,7 +566,7 @@ static void launch_xtile(XTile xt, int num_sms, cudaStream_t st, const double* S
 __global__ void k_gather(const MgRow* __restrict__ rows, const double* __restrict__ G,
                          const int* __restrict__ modes, const double* __restrict__ q, int L,
                          int l_min, int p, int P2, int nm, int n3, int64_t kp,
-                         double* __restrict__ RB, double* __restrict__ SqB) {
+                         double* __restrict__ RB, double* __restrict__ SqB, MgBounds bd) {
     // Blocked, smem-identical layouts of the pair contraction's operands (one bulk copy per
     // stage): RB[nt][r][RUN_LDB] (column c = nt*RUN_TN + cn), SqB[mt][r][RUN_LDA] (pair
     // pr = mt*RUN_TM + m).  Rows r in [n3, gridDim.y) are the zero K-padding of the last tile.
@@ -536,6 +587,7 @@ __global__ void k_gather(const MgRow* __restrict__ rows, const double* __restric
                   Gr[(int64_t)(cp + a) * P2 + pair_idx(b, d)];
         }
         const int nt = idx / RUN_TN, cn = idx - nt * RUN_TN;
+        MG_DCHECK(in_range(((int64_t)nt * kp + r) * RUN_LDB + cn, 1, bd.r), CK_GATHER_W);
         RB[((int64_t)nt * kp + r) * RUN_LDB + cn] = val;
     }
     if (blockIdx.x == 0) {
@@ -550,6 +602,7 @@ __global__ void k_gather(const MgRow* __restrict__ rows, const double* __restric
                 s = qa[w.l2] * qb[w.l3] + qb[w.l2] * qa[w.l3];
             }
             const int mt = pr / RUN_TM, m = pr - mt * RUN_TM;
+            MG_DCHECK(in_range(((int64_t)mt * kp + r) * RUN_LDA + m, 1, bd.sq), CK_GATHER_W);
             SqB[((int64_t)mt * kp + r) * RUN_LDA + m] = s;
         }
     }
@@ -562,6 +615,7 @@ __global__ void k_gather(const MgRow* __restrict__ rows, const double* __restric
 // tile and pipeline; stages are one bulk copy of SqB and one of RB.
 struct PairItems {
     static constexpr bool kComputeA = false;
+    MgBounds bd;
     const double* SqB;
     const double* RB;
     int64_t kp;
@@ -598,21 +652,24 @@ struct PairItems {
         int s, mt, nt;
         decode(it, s, mt, nt);
         const int64_t r = (int64_t)s * per + kt * RUN_BK;
-        if (lane == 0)
+        if (lane == 0) {
+            MG_DCHECK(in_range(((int64_t)mt * kp + r) * RUN_LDA, RUN_BK * RUN_LDA, bd.sq), CK_K3_SQ);
             bulk_g2s(As, SqB + ((int64_t)mt * kp + r) * RUN_LDA,
                      RUN_BK * RUN_LDA * sizeof(double), bar);
-        else
+        } else {
+            MG_DCHECK(in_range(((int64_t)nt * kp + r) * RUN_LDB, RUN_BK * RUN_LDB, bd.r), CK_K3_R);
             bulk_g2s(Bs, RB + ((int64_t)nt * kp + r) * RUN_LDB,
                      RUN_BK * RUN_LDB * sizeof(double), bar);
+        }
     }
 };
 
 __global__ void __launch_bounds__(RunPipeP::THREADS, 1)
 k_pair_contract(const double* __restrict__ SqB, const double* __restrict__ RB, int64_t kp,
                 int n3, int per, int nsplit, int P2, int ncols, int64_t zsplit,
-                double* __restrict__ Z) {
+                double* __restrict__ Z, MgBounds bd) {
     extern __shared__ __align__(16) double smem[];
-    PairItems items{SqB, RB, kp, n3, per, (P2 + RUN_TM - 1) / RUN_TM,
+    PairItems items{bd, SqB, RB, kp, n3, per, (P2 + RUN_TM - 1) / RUN_TM,
                     (ncols + RUN_TN - 1) / RUN_TN, P2, ncols};
     const int nitems = nsplit * items.MT * items.NT;
     RunPipeP::run(blockIdx.x, gridDim.x, nitems, items, [&](int it, const Acc<CfgRun>& acc) {
@@ -624,6 +681,7 @@ k_pair_contract(const double* __restrict__ SqB, const double* __restrict__ RB, i
             const int prr = m0 + m, c = n0 + n;
             if (prr < P2) {
                 double* z = Zs + (int64_t)prr * ncols;
+                MG_DCHECK(c >= ncols || in_range(z + c - Z, c + 1 < ncols ? 2 : 1, bd.z), CK_K3_Z_W);
                 if (c < ncols) z[c] += v0;
                 if (c + 1 < ncols) z[c + 1] += v1;
             }
@@ -655,6 +713,25 @@ __global__ void k_final(const double* __restrict__ Z, int nsplit, int64_t zsplit
 // host side
 // ------------------------------------------------------------------------------------------
 
+// Counters of the checked build's bounds checks, per site (MgCheck); zeros in a normal build.
+int debug_checks(uint32_t* out, int n, bool reset) {
+    for (int i = 0; i < n; ++i) out[i] = 0;
+#if MG_CHECKED
+    unsigned int h[16] = {0};
+    MG_CUDA(cudaDeviceSynchronize());
+    MG_CUDA(cudaMemcpyFromSymbol(h, g_chk, sizeof(h)));
+    for (int i = 0; i < n && i < 16; ++i) out[i] = h[i];
+    if (reset) {
+        const unsigned int z[16] = {0};
+        MG_CUDA(cudaMemcpyToSymbol(g_chk, z, sizeof(z)));
+    }
+    return 1;
+#else
+    (void)reset;
+    return 0;
+#endif
+}
+
 std::vector<double> log_factorials(int n) {
     // t[k] = log(k!) accumulated left to right like np.cumsum(np.log(arange(1, size)))
     std::vector<double> t(n + 1, 0.0);
@@ -668,7 +745,9 @@ void plan_init(mg_plan* P, const double* q, const double* qt_host, const double*
     MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
     MG_REQUIRE(p >= 1 && Nx >= 1 && n >= 1, "p, Nx, n must be >= 1");
     MG_REQUIRE(h2_mode == MG_H2_GOSPER || h2_mode == MG_H2_EXACT, "unknown h2_mode");
-    MG_REQUIRE(p <= 32, "p_max > 32 not supported");
+    // (row, c) slot division by multiply-shift is exact for p < 197 (slot + c0 < p + 128);
+    // beyond that the per-row operands (G: p^4/2 doubles, Z: p^3 n) outgrow HBM anyway
+    MG_REQUIRE(p <= 196, "p_max > 196 not supported");
     const int L = l_max - l_min + 1;
     for (int i = 0; i < L; ++i) {
         MG_REQUIRE(C[i] > 0, "power spectrum C_l must be strictly positive");
@@ -991,6 +1070,10 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     const int64_t zsplit = (int64_t)P2 * ncols;
     P->sc->Z.ensure((size_t)nsplit * zsplit);
     P->gamma.ensure((size_t)nm * nm);
+    // buffer extents for the checked build's bounds checks (MG_CHECKED; free otherwise)
+    const MgBounds bd{maxpanel, (int64_t)P->WQT.n, (int64_t)P->sc->H.n, (int64_t)P->sc->S.n,
+                      (int64_t)P->sc->G.n, (int64_t)P->sc->R.n, (int64_t)P->sc->Sq.n,
+                      (int64_t)P->sc->Z.n, 0, 0};
 
     static bool attr_done_dev[64] = {false};  // function attributes are per device context
     bool& attr_done = attr_done_dev[P->device & 63];
@@ -1061,7 +1144,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
                        os>>>(
             P->prep.tiles_d.p + tf, P->prep.rows.p, P->prep.poff.p + tf, P->prep.zoff.p, zbase,
             zt, P->l0d.p, P->q.p, P->L, P->l_min, p, P->C.p, P->v.p, P->lf.p, P->fl.p,
-            P->h2_mode, panel_buf[k & 1], (65536u + p - 1) / p);
+            P->h2_mode, panel_buf[k & 1], (65536u + p - 1) / p, bd);
         MG_LAUNCHED();
     };
 
@@ -1069,7 +1152,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         const Batch& B = batches[k];
         dim3 gs(ceil_div(P2, PP_CHUNK), (int)(B.e1 - B.b1));
         k_pair_products<<<gs, MG_PP_THREADS, 0, os>>>(P->prep.rows.p, (int)B.b1, P->QT.p, p, P2, NxP,
-                                             P->l_min, P->sc->S.p);
+                                             P->l_min, P->sc->S.p, bd);
         MG_LAUNCHED();
     };
 
@@ -1116,7 +1199,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
             P->prep.rows.p, P->WQT.p, p, P->Nx, P->Nxw, NxP,
             make_longlong2(P->wbase[0], P->wbase[1]), make_int2(P->wrows[0], P->wrows[1]),
             P->sc->H.p, (65536u + p - 1) / p,
-            (unsigned)(((1ull << 32) + P->Nxw - 1) / P->Nxw));
+            (unsigned)(((1ull << 32) + P->Nxw - 1) / P->Nxw), bd);
         MG_LAUNCHED();
 #if MG_SIDE
         prof_mark(P, 0, ms);
@@ -1124,7 +1207,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
 #endif
         prof_mark(P, 2, ms);
         launch_xtile(xt, num_sms, ms, P->sc->S.p, P->sc->H.p, nb, (int)B.b1, (int)B.b3, p, P2,
-                     P->Nx, NxP, P->sc->G.p);
+                     P->Nx, NxP, P->sc->G.p, bd);
         MG_LAUNCHED();
         MG_CUDA(cudaEventRecord(P->ev_x, ms));
         launches += 4 + (dt1 ? 1 : 0);
@@ -1139,13 +1222,13 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         prof_mark(P, 3, ms);
         dim3 gg(std::min(ceil_div(ncols, 256), 64), (int)round_up(n3, RUN_BK));
         k_gather<<<gg, 256, 0, ms>>>(P->prep.rows.p + B.b3, P->sc->G.p, P->modes.p, P->q.p, P->L,
-                                     P->l_min, p, P2, nm, n3, kp, P->sc->R.p, P->sc->Sq.p);
+                                     P->l_min, p, P2, nm, n3, kp, P->sc->R.p, P->sc->Sq.p, bd);
         MG_LAUNCHED();
         const int per = (int)round_up(ceil_div(n3, nsplit), RUN_BK);
         prof_mark(P, 4, ms);
         k_pair_contract<<<num_sms, RunPipeP::THREADS, smem_run, ms>>>(
             P->sc->Sq.p, P->sc->R.p, kp, n3, per, ceil_div(n3, per), P2, ncols, zsplit,
-            P->sc->Z.p);
+            P->sc->Z.p, bd);
         MG_LAUNCHED();
         launches += 2;
         f_pair += 2.0 * P2 * ncols * (double)n3;
@@ -1665,7 +1748,7 @@ __global__ void __launch_bounds__(NSD_THREADS, 1)
 k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int64_t count,
               const double* __restrict__ QTS, const double* __restrict__ Q1W, int XB8,
               const NsAfrag<PP> af, const double* __restrict__ q, const int* __restrict__ modes,
-              int P, int nm, int L, int l_min, double* __restrict__ partial) {
+              int P, int nm, int L, int l_min, double* __restrict__ partial, MgBounds bd) {
     using SG = NsStage<PP>;
     constexpr int NK = ns_groups<PP>(), CH = NS_CH, NST = NS_ST, CHUNK = SG::CHUNK;
     constexpr int NW = NSD_THREADS / 32;
@@ -1710,6 +1793,12 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
         const int c0 = ps * CH, nch = min(CH, XB8 - c0);
         const uint32_t bytes = (uint32_t)nch * CHUNK * 8;
         double* st = stg + (size_t)slot * SG::DOUBLES;
+        MG_DCHECK(ptr.x >= l_min && ptr.y >= ptr.x && ptr.z >= ptr.y && ptr.z - l_min < L, CK_NS_L);
+        MG_DCHECK(in_range((ptr.y - l_min) * lstride + (int64_t)c0 * CHUNK, (int64_t)nch * CHUNK,
+                           bd.qts) &&
+                      in_range((ptr.z - l_min) * lstride + (int64_t)c0 * CHUNK,
+                               (int64_t)nch * CHUNK, bd.qts),
+                  CK_NS_QTS);
         mbar_arrive_expect_tx(full + slot, 2 * bytes);
         bulk_g2s(st, QTS + (ptr.y - l_min) * lstride + (int64_t)c0 * CHUNK, bytes, full + slot);
         bulk_g2s(st + CH * CHUNK, QTS + (ptr.z - l_min) * lstride + (int64_t)c0 * CHUNK, bytes,
@@ -1734,7 +1823,6 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
             mbar_wait(full + slot, (int)((gst / NST) & 1));
             const double* st = stg + (size_t)slot * SG::DOUBLES;
             const int nch = min(CH, XB8 - s * CH);
-#pragma unroll
             // All NS_CH chunks of the stage at once: their pair products S first (each chunk's
             // rotated q̃ rows are dead once its 9 S values exist), then the DMMAs of the
             // NS_CH independent accumulator chains interleaved k-step by k-step, so a warp
@@ -1774,6 +1862,8 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
             const double* b1 = p1 + (int64_t)s * CH * CHUNK;
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
+                MG_DCHECK(!(u < nch && g < PP) || in_range(b1 + u * CHUNK - Q1W, 2, bd.q1w),
+                          CK_NS_Q1W);
                 const double2 w = (u < nch && g < PP)
                                       ? __ldg(reinterpret_cast<const double2*>(b1 + u * CHUNK))
                                       : make_double2(0.0, 0.0);
@@ -1843,7 +1933,8 @@ static void launch_nonsep_dmma(mg_plan* Pl, const std::vector<double>& at, cudaS
     k_nonsep_dmma<PP><<<Pl->ns_blocks, NSD_THREADS, shm, st>>>(
         reinterpret_cast<const int4*>(Pl->ns_trip.p), Pl->ns_wz.p, Pl->ns_count, Pl->ns_qt2.p,
         Pl->ns_q1w.p, XB8, af, Pl->q.p, Pl->modes.p, Pl->p, Pl->nm, Pl->L, Pl->l_min,
-        Pl->ns_part.p);
+        Pl->ns_part.p,
+        MgBounds{0, 0, 0, 0, 0, 0, 0, 0, (int64_t)Pl->ns_qt2.n, (int64_t)Pl->ns_q1w.n});
 }
 
 template <int P>
@@ -1959,6 +2050,7 @@ void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_ho
                 P->ns_alpha.upload(alpha, nm, st);
                 const size_t shm = (size_t)nm * 8 + NS_THREADS / 32 * 8 + (3 * nm + 1) * 4 + 8 +
                                    (size_t)nm * 8;
+                MG_REQUIRE(shm <= 227 * 1024, "too many modes for the non-separable path");
                 MG_CUDA(cudaFuncSetAttribute(k_nonsep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)std::max<size_t>(shm, 48 * 1024)));
                 k_nonsep<<<P->ns_blocks, NS_THREADS, shm, st>>>(

@@ -135,4 +135,5 @@ void nonsep(mg_plan* P, const double* alpha, const int32_t* l1, const int32_t* l
 void weights(int l_min, int l_max, const double* C, const double* v, int h2_mode,
              int64_t begin, int64_t end, double* zm, int32_t* o1, int32_t* o2, int32_t* o3);
 std::vector<double> log_factorials(int n);
+int debug_checks(uint32_t* out, int n, bool reset);
 }  // namespace mg

@@ -340,7 +340,9 @@ void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x
                       double* delta_out_dev, cudaStream_t s) {
     MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
     MG_REQUIRE(Nk >= 1 && Nx >= 1 && p >= 1, "Nk, Nx, p must be >= 1");
-    MG_REQUIRE(p * QB_XT * QB_LT <= 4 * QB_KT, "p_max too large for the q-tilde kernel (<= 32)");
+    // the sweep kernel holds up to QB_PMAX components (4 DMMA m-fragments); larger bases are
+    // built in component blocks (each block re-runs the Bessel recurrences)
+    constexpr int QB_PMAX = 4 * QB_KT / (QB_XT * QB_LT);
     for (int i = 0; i < Nk; ++i) MG_REQUIRE(k[i] > 0, "k grid must be > 0");
     const int L = l_max - l_min + 1;
     DBuf<double> dk, dwk, dx, deps, dqk, ddelta, db;
@@ -367,19 +369,24 @@ void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x
         DBuf<double> ua(np), ub(np), da(np), dbb(np), nrm(np);
         DBuf<int> ds(np), lsw(np), stot(np);
         QState st{ua.p, ub.p, da.p, dbb.p, ds.p, nrm.p, lsw.p, stot.p};
-        k_qb_prepare<<<(int)std::min<size_t>((np + 255) / 256, 148 * 64), 256, 0, s>>>(
-            dk.p, Nk, dx.p, Nx, l_min, l_max, st);
-        MG_LAUNCHED();
-        const int mf = (p + 7) / 8;
-        const size_t shm =
-            (size_t)(QB_LT * QB_XT * QB_LDU + (MG_QB_DMMA ? mf * 8 : p) * QB_LDB) * sizeof(double);
         const int grid = (Nx + QB_XT - 1) / QB_XT;
-        for (int dir : {+1, -1}) {
-            switch (MG_QB_DMMA ? mf : 1) {
-                case 1: launch_qb_sweep<1>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max, st, qt_dev); break;
-                case 2: launch_qb_sweep<2>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max, st, qt_dev); break;
-                case 3: launch_qb_sweep<3>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max, st, qt_dev); break;
-                default: launch_qb_sweep<4>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, db.p, p, l_min, l_max, st, qt_dev); break;
+        for (int c0 = 0; c0 < p; c0 += QB_PMAX) {  // component blocks: qt is [p][Nx][L]
+            const int pb = std::min(QB_PMAX, p - c0);
+            const double* bb = db.p + (size_t)c0 * Nk;
+            double* qo = qt_dev + (size_t)c0 * Nx * L;
+            k_qb_prepare<<<(int)std::min<size_t>((np + 255) / 256, 148 * 64), 256, 0, s>>>(
+                dk.p, Nk, dx.p, Nx, l_min, l_max, st);
+            MG_LAUNCHED();
+            const int mf = (pb + 7) / 8;
+            const size_t shm = (size_t)(QB_LT * QB_XT * QB_LDU + (MG_QB_DMMA ? mf * 8 : pb) * QB_LDB) *
+                               sizeof(double);
+            for (int dir : {+1, -1}) {
+                switch (MG_QB_DMMA ? mf : 1) {
+                    case 1: launch_qb_sweep<1>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, bb, pb, l_min, l_max, st, qo); break;
+                    case 2: launch_qb_sweep<2>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, bb, pb, l_min, l_max, st, qo); break;
+                    case 3: launch_qb_sweep<3>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, bb, pb, l_min, l_max, st, qo); break;
+                    default: launch_qb_sweep<4>(grid, shm, s, dir, dk.p, Nk, dx.p, Nx, delta, bb, pb, l_min, l_max, st, qo); break;
+                }
             }
         }
         MG_CUDA(cudaStreamSynchronize(s));  // temporaries die with this scope

@@ -449,3 +449,35 @@ class TestMultiDevice:
         a = gamma3d_matrix(t, m, r, domain=dd, devices=[0]).values
         b = gamma3d_matrix(t, m, r, domain=dd, devices=[0, 0]).values
         assert frob_rel(b, a) < 1e-12
+
+
+def test_large_basis_beyond_32():
+    """p_max = 40 (> 32: the reference accepts any p_max, basis.py:57-94): stage 1 in
+    component blocks vs scipy, and the separable Γ on a 160-mode subset mapping vs the
+    oracle (P2 = 820 pairs, p^2 = 1600 (c,c') columns, several M/N tiles per row)."""
+    from dataclasses import replace
+    from oracle import qtilde_ref
+    from paper_1503_08809_b200 import build_qtilde, default_mode_mapping
+    from paper_1503_08809_b200.basis import legendre_on_interval, shifted_legendre
+    p = 40
+    hi = host_inputs("c0", l_max=48)
+    qk = legendre_on_interval(p, hi.k, hi.spec.k_range[0],
+                              hi.spec.k_range[1] - hi.spec.k_range[0])
+    hi = replace(hi, qk=qk, q=shifted_legendre(p, 2, 48))
+    C, qt = build_qtilde(hi)
+    d = qtilde_ref.delta_table(hi.k, hi.eps, 2, 48)
+    ells = [2, 25, 48]
+    want = qtilde_ref.qtilde(hi.k, hi.wk, hi.x, hi.qk, d, 2, 48, ells)
+    for l in ells:
+        a, b = qt[:, :, l - 2], want[:, :, l - 2]
+        assert np.linalg.norm(a - b) <= 1e-11 * np.linalg.norm(b), l
+    full = default_mode_mapping(p).entries
+    rng = np.random.default_rng(4)
+    sub = full[np.unique(np.concatenate([[0, full.shape[0] - 1],
+                                         rng.choice(full.shape[0], 158, replace=False)]))]
+    t = BasisTables(hi.q, qt, C, hi.v, 2, 48)
+    m = ModeMapping(sub, p)
+    got = gamma3d_matrix(t, m, RadialGrid(hi.x)).values
+    ref_g = ref.gamma3d(hi.q, qt, C, hi.v, hi.wr2, sub, 2, 48, workers=8, block=32)
+    assert got.shape == (sub.shape[0], sub.shape[0])
+    assert frob_rel(got, ref_g) < 1e-12

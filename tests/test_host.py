@@ -230,3 +230,24 @@ def test_integration_shim_rebinds_reference_names():
     after = (cp.gamma3d_matrix, cp.engine3d.gamma3d_matrix, cp.harness.gamma3d_matrix,
              cp.gamma2d_matrix, cp.engine2d.gamma2d_matrix, cp.harness.gamma2d_matrix)
     assert all(a is b for a, b in zip(before, after))
+
+
+def test_shape_checks_before_the_c_call():
+    """The C-ABI reads raw pointers, so the drop-ins reject inconsistent shapes up front
+    (a radial grid whose length differs from q̃'s n_radial would otherwise be read out of
+    bounds): ValueError like the reference's einsum / BasisTables validation."""
+    from paper_1503_08809_b200 import BasisTables, GammaPlan, ModeMapping, RadialGrid
+    from paper_1503_08809_b200.quadrature import x_weights
+    L, p, nx = 15, 3, 20
+    rng = np.random.default_rng(0)
+    t = BasisTables(rng.standard_normal((p, L)), rng.standard_normal((p, nx, L)),
+                    rng.uniform(1, 2, L), np.ones(L), 2, 16)
+    m = mg.default_mode_mapping(p)
+    short = RadialGrid(np.linspace(1.0, 2.0, nx - 3))
+    with pytest.raises(ValueError, match="n_radial"):
+        mg.gamma3d_matrix(t, m, short, devices=[0])
+    with pytest.raises(ValueError, match="n_radial"):
+        mg.gamma_nonsep(t, m, short, np.ones(m.n_max),
+                        mg.SparseDomain([2], [2], [2], [1.0]))
+    with pytest.raises(ValueError):
+        GammaPlan(t.q, t.q_tilde, t.C, t.v, x_weights(short.r), m.entries, 2, 16)
