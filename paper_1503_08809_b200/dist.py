@@ -82,11 +82,21 @@ def gamma3d_matrix_distributed(tables, mapping, grid, h2_mode="gosper", integrat
         import os
         # the rank's own GPU on its node (LOCAL_RANK), never the global rank
         dev = int(os.environ.get("LOCAL_RANK", "0")) if device is None else int(device)
-        part = slab_partial(tables, mapping, wr2, a, b, h2_mode, dev)
-        use_cuda = dist.get_backend(group) == "nccl"
-        t = torch.from_numpy(part)
-        if use_cuda:
-            t = t.to(torch.device("cuda", dev))
+        if dist.get_backend(group) == "nccl":
+            # partial Γ stays in device memory for the NCCL exchange (no host round trip)
+            from .plan import GammaPlan
+            n = mapping.n_max
+            t = torch.empty((n, n), dtype=torch.float64, device=torch.device("cuda", dev))
+            plan = GammaPlan.from_tables(tables, mapping, grid, h2_mode, integrator, device=dev)
+            try:
+                with torch.cuda.device(dev):
+                    s = torch.cuda.current_stream()
+                    plan.execute(a, b, out=t, stream=s)
+                    s.synchronize()
+            finally:
+                plan.close()
+        else:
+            t = torch.from_numpy(slab_partial(tables, mapping, wr2, a, b, h2_mode, dev))
     else:
         t = torch.from_numpy(np.ascontiguousarray(partial_fn(tables, mapping, wr2, a, b,
                                                              h2_mode)))

@@ -481,3 +481,30 @@ def test_large_basis_beyond_32():
     ref_g = ref.gamma3d(hi.q, qt, C, hi.v, hi.wr2, sub, 2, 48, workers=8, block=32)
     assert got.shape == (sub.shape[0], sub.shape[0])
     assert frob_rel(got, ref_g) < 1e-12
+
+
+def test_distributed_nccl_path_world1(g_c0):
+    """The torchrun path (dist.gamma3d_matrix_distributed) with a real NCCL communicator:
+    partial Γ written by the plan straight into device memory, all-gathered over NCCL and
+    summed in rank order (world size 1 on one GPU; the N > 1 host logic is the gloo test)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1503_08809_b200.dist import gamma3d_matrix_distributed
+    hi = host_inputs("c0")
+    t = BasisTables(hi.q, g_c0["qt"], g_c0["C"], hi.v, 2, 200)
+    m, r = ModeMapping(hi.entries, 6), RadialGrid(hi.x)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        g = gamma3d_matrix_distributed(t, m, r, device=0)
+    finally:
+        dist.destroy_process_group()
+    assert g.meta["ranks"] == 1
+    assert frob_rel(g.values, g_c0["gamma"]) < 1e-10
+    assert frob_rel(g.values, gamma3d_matrix(t, m, r, devices=[0]).values) < 1e-13
