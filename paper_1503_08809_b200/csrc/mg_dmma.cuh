@@ -480,6 +480,141 @@ struct PipeTMAPersistent {
     }
 };
 
+// N-split form of the persistent pipeline, for tiles whose last N tile is mostly padding
+// (p = 15 x contraction: N = 225 = 128 + 97).  The item's valid n-fragments nfr (of
+// FN * WARPS_N) are dealt to the WARPS_N warp columns as evenly as possible, so a warp owns
+// FN or FN - 1 n-fragments (one warp-uniform dispatch per item into two compiled loop bodies:
+// no per-DMMA predicates) starting at a per-item column offset.  Warp columns are rotated by
+// the warp row (wn = (warp + warp / WARPS_N) % WARPS_N), so the warps with the extra fragment
+// fall on different SM sub-partitions (warp % 4) and the four DMMA units stay balanced:
+// 13 n-fragments run as 4,3,3,3 -> 50 fragment-steps per sub-partition instead of 60.
+// Extra producer contract: int nfrags(int it) (valid n-fragments of the item, each warp
+// column must get FN or FN - 1); the epilogue is epi(it, acc, wm, wn, nf).
+template <class Cfg, int BK, int STAGES, bool AK, bool BKM>
+struct PipeTMAPersistentNS {
+    using Base = PipeTMA<Cfg, BK, STAGES, AK, BKM>;
+    static constexpr int WARPS = Base::WARPS, THREADS = Base::THREADS;
+    static constexpr int SA = Base::SA, SB = Base::SB, SS = Base::SS;
+    static constexpr size_t smem_bytes = Base::smem_bytes;
+
+    template <int NF, class Prod>
+    __device__ __forceinline__ static void item_loop(const Prod& prod, double* smem,
+                                                     uint64_t* full, uint64_t* empty, int kts,
+                                                     int kvl, int wm, int wn, int& g,
+                                                     Acc<Cfg>& acc) {
+        constexpr int FM = Cfg::FM;
+        const int lane = threadIdx.x & 31;
+        const int g4 = lane >> 2, t = lane & 3;
+        // B fragments are double-buffered in registers; each A fragment is reloaded for the next
+        // k4 step right after its own row of DMMAs has been issued (a warp's k4 steps are
+        // hundreds of pipe cycles apart with three warps per DMMA unit, so the reload latency
+        // is covered) — 13 fragment doubles instead of 18, which keeps the 5 x 4 tile's 40
+        // accumulators inside the 128 registers a 13-warp CTA can allocate.
+        double a[FM], b[2][NF];
+        auto load_b = [&](int buf, const double* Bs, int k) {
+#pragma unroll
+            for (int ni = 0; ni < NF; ++ni)
+                b[buf][ni] = frag_ld<BKM, Cfg::BN, BK>(Bs, k, wn + ni * 8 + g4);
+        };
+        {
+            const int s = g % STAGES;
+            mbar_wait(full + s, (g / STAGES) & 1);
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
+                a[mi] = frag_ld<AK, Cfg::BM, BK>(smem + s * SS, t, wm + mi * 8 + g4);
+            load_b(0, smem + s * SS + SA, t);
+        }
+        for (int kt = 0; kt < kts; ++kt, ++g) {
+            const int s = g % STAGES, s2 = (g + 1) % STAGES;
+            const int ph2 = ((g + 1) / STAGES) & 1;
+            const double* As = smem + s * SS;
+            const double* Bs = As + SA;
+            const double* As2 = smem + s2 * SS;
+            const double* Bs2 = As2 + SA;
+            const bool more = kt + 1 < kts;
+            const int nks = more ? BK / 4 : (kvl + 3) / 4;
+            uint32_t ready = more ? mbar_test(full + s2, ph2) : 1u;
+#pragma unroll
+            for (int ks = 0; ks < BK / 4; ++ks) {
+                if (ks < nks) {
+                    const int cur = ks & 1;
+                    // source of the next k4 step's fragments: this stage, the next stage, none
+                    const bool in_stage = ks + 1 < BK / 4;
+                    const bool next = in_stage || more;
+                    if (!in_stage && more && !ready) mbar_wait(full + s2, ph2);
+                    const double* An = in_stage ? As : As2;
+                    const double* Bn = in_stage ? Bs : Bs2;
+                    const int kn = in_stage ? (ks + 1) * 4 + t : t;
+                    if (next) load_b(cur ^ 1, Bn, kn);
+#pragma unroll
+                    for (int mi = 0; mi < FM; ++mi) {
+#pragma unroll
+                        for (int ni = 0; ni < NF; ++ni) dmma884(acc.c[mi][ni], a[mi], b[cur][ni]);
+                        if (next) a[mi] = frag_ld<AK, Cfg::BM, BK>(An, kn, wm + mi * 8 + g4);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+    }
+
+    template <class Prod, class Epi>
+    __device__ static void run(int first, int stride, int nitems, const Prod& prod, Epi&& epi,
+                               double* smem) {
+        constexpr int FM = Cfg::FM, FN = Cfg::FN, WN = Cfg::WARPS_N;
+        static_assert((BK / 4) % 2 == 0, "cross-stage fragment prefetch needs an even k4 count");
+        static_assert(FN >= 2, "a warp column owns FN or FN - 1 fragments");
+        uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SS);
+        uint64_t* empty = full + STAGES;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(full + s, 1);
+                mbar_init(empty + s, WARPS);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        }
+        __syncthreads();
+        if (warp == WARPS) {  // ---------------- producer warp
+            int g = 0;
+            for (int it = first; it < nitems; it += stride) {
+                const int kts = prod.ktiles(it);
+                for (int kt = 0; kt < kts; ++kt, ++g) {
+                    const int s = g % STAGES;
+                    if (g >= STAGES) mbar_wait(empty + s, ((g / STAGES) - 1) & 1);
+                    double* st = smem + s * SS;
+                    if (lane == 0) mbar_arrive_expect_tx(full + s, prod.stage_bytes(it, kt));
+                    __syncwarp();
+                    prod.bulk_rows(it, kt, st, st + SA, lane, full + s);
+                }
+            }
+            return;
+        }
+        // ------------------------------------------------------------- consumer warps
+        const int wmi = warp / WN, wni = (warp + wmi) % WN;
+        const int wm = wmi * (8 * FM);
+        Acc<Cfg> acc;
+        int g = 0;
+        for (int it = first; it < nitems; it += stride) {
+#pragma unroll
+            for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni) acc.c[mi][ni][0] = acc.c[mi][ni][1] = 0.0;
+            const int kts = prod.ktiles(it), kvl = prod.kvalid_last(it);
+            const int nfr = prod.nfrags(it);
+            const int base = nfr / WN, rem = nfr - base * WN;
+            const int nf = base + (wni < rem ? 1 : 0);
+            const int wn = 8 * (wni * base + min(wni, rem));
+            if (nf == FN)
+                item_loop<FN>(prod, smem, full, empty, kts, kvl, wm, wn, g, acc);
+            else
+                item_loop<FN - 1>(prod, smem, full, empty, kts, kvl, wm, wn, g, acc);
+            epi(it, acc, wm, wn, nf);
+        }
+    }
+};
+
 // Visit every accumulator element: f(m_local, n_local, v(n), v(n+1)).
 template <class Cfg, class F>
 __device__ __forceinline__ void acc_foreach_pair(const Acc<Cfg>& acc, F&& f) {

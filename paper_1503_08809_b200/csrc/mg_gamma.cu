@@ -424,8 +424,11 @@ struct XItems {
     const double* S;
     const double* H;
     int P2, pp, XB, MT, NT, kv_last;
+    int flip = 0;  // N-split tiles: rotate nt every `flip` items (a multiple of NT) so a CTA
+                   // striding by the grid size alternates between full and partial N tiles
     __device__ void decode(int it, int& r, int& mt, int& nt) const {
         nt = it % NT;
+        if (flip) nt = (nt + it / flip) % NT;
         mt = (it / NT) % MT;
         r = it / (NT * MT);
     }
@@ -435,6 +438,11 @@ struct XItems {
         int r, mt, nt;
         decode(it, r, mt, nt);
         return make_int2(min(Cfg::BM, P2 - mt * Cfg::BM), min(Cfg::BN, pp - nt * Cfg::BN));
+    }
+    __device__ int nfrags(int it) const {  // valid n-fragments of the item's N tile
+        int r, mt, nt;
+        decode(it, r, mt, nt);
+        return (min(Cfg::BN, pp - nt * Cfg::BN) + 7) / 8;
     }
     __device__ uint32_t stage_bytes(int it, int) const {
         int r, mt, nt;
@@ -493,6 +501,47 @@ k_x_contract_p(const double* __restrict__ S, const double* __restrict__ H, int n
     }, smem);
 }
 
+// N-split x contraction (PipeTMAPersistentNS): 120 x 128 tile on 12 consumer warps of 5 x 4
+// fragments; the partial last N tile deals its valid n-fragments over the four warp columns
+// (p = 15: 225 columns = 16 + 13 n-fragments -> warps run 4 or 3 n-fragments).
+template <class Cfg>
+using XPipeNS = PipeTMAPersistentNS<Cfg, X_BK, 3, false, false>;
+
+template <class Cfg>
+__global__ void __launch_bounds__(XPipeNS<Cfg>::THREADS, 1)
+k_x_contract_ns(const double* __restrict__ S, const double* __restrict__ H, int nrows,
+                int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* __restrict__ G,
+                MgBounds bd) {
+    extern __shared__ __align__(16) double smem[];
+    const int pp = p * p;
+    XItems<Cfg> items{bd, S, H, P2, pp, NxP / X_BK, (P2 + Cfg::BM - 1) / Cfg::BM,
+                      (pp + Cfg::BN - 1) / Cfg::BN, 0};
+    items.kv_last = Nx - (items.XB - 1) * X_BK;
+    items.flip = (int)gridDim.x % items.NT == 0 ? (int)gridDim.x : 0;
+    const int nitems = nrows * items.MT * items.NT;
+    XPipeNS<Cfg>::run(blockIdx.x, gridDim.x, nitems, items,
+                      [&](int it, const Acc<Cfg>& acc, int wm, int wn, int nf) {
+        int r, mt, nt;
+        items.decode(it, r, mt, nt);
+        const int lane = threadIdx.x & 31;
+        const int m0 = mt * Cfg::BM + wm + (lane >> 2), n0 = nt * Cfg::BN + wn + 2 * (lane & 3);
+        double* Gr = G + (int64_t)(row_b1 + r - row_b3) * pp * P2;
+#pragma unroll
+        for (int mi = 0; mi < Cfg::FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < Cfg::FN; ++ni) {
+                const int prr = m0 + mi * 8, cc = n0 + ni * 8;
+                if (ni < nf && prr < P2 && !MG_NO_EPI) {
+                    MG_DCHECK(cc >= pp || in_range(Gr + (int64_t)cc * P2 + prr - G, 1, bd.g), CK_K2_G_W);
+                    MG_DCHECK(cc + 1 >= pp || in_range(Gr + (int64_t)(cc + 1) * P2 + prr - G, 1, bd.g),
+                              CK_K2_G_W);
+                    if (cc < pp) Gr[(int64_t)cc * P2 + prr] = acc.c[mi][ni][0];
+                    if (cc + 1 < pp) Gr[(int64_t)(cc + 1) * P2 + prr] = acc.c[mi][ni][1];
+                }
+            }
+    }, smem);
+}
+
 // x-contraction tiles.  The CTA tile is chosen per basis size from M = p(p+1)/2 pairs and
 // N = p^2 (c,c') columns (choose_xtile).  Consumer warps are 12 (3 per SM sub-partition: every
 // DMMA unit serves the same number of warps; 13 warps allocate up to 128 registers) or 15
@@ -508,8 +557,34 @@ using CfgX120x96 = TileCfg<3, 4, 5, 3>;
 using CfgX128x72 = TileCfg<4, 3, 4, 3>;
 using CfgX160x72 = TileCfg<4, 3, 5, 3>;
 using CfgX128 = TileCfg<2, 4, 8, 4>;
+//   T120x128NS 120 x 128, 12 warps, 5x4 fragments, N-split (k_x_contract_ns)
+//                                                            p = 15: 225 = 16 + 13 n-fragments
+using CfgX120x128 = TileCfg<3, 4, 5, 4>;
 
-enum class XTile { T120 = 0, T120x96, T128x72, T160x72, T128, COUNT };
+enum class XTile { T120 = 0, T120x96, T128x72, T160x72, T128, T120x128NS, COUNT };
+
+// DMMA-pipe model of the N-split tile: fragment-steps of the busiest SM sub-partition per row
+// (sub-partition s = warp % 4 holds warp rows 0..2 with warp columns s, s+1, s+2 mod 4) against
+// the useful ones; 0 when a warp column would get fewer than FN - 1 fragments.
+static double nsplit_efficiency(int P2, int pp) {
+    using C = CfgX120x128;
+    const int MT = ceil_div(P2, C::BM), NT = ceil_div(pp, C::BN);
+    double cost = 0.0;
+    for (int nt = 0; nt < NT; ++nt) {
+        const int nfr = (std::min(C::BN, pp - nt * C::BN) + 7) / 8;
+        const int base = nfr / C::WARPS_N, rem = nfr % C::WARPS_N;
+        if (base + (rem ? 1 : 0) > C::FN || base < C::FN - 1) return 0.0;
+        int worst = 0;
+        for (int s = 0; s < 4; ++s) {
+            int load = 0;
+            for (int wmi = 0; wmi < C::WARPS_M; ++wmi)
+                load += C::FM * (base + (((s + wmi) % C::WARPS_N) < rem ? 1 : 0));
+            worst = std::max(worst, load);
+        }
+        cost += worst;
+    }
+    return ((double)P2 * pp / 64.0 / 4.0) / (cost * MT);
+}
 
 // Padded-area efficiency of M = P2, N = pp on a bm x bn tile, times a per-tile pipe factor
 // (sub-partition balance / measured DMMA-pipe utilisation).  MG_XTILE=<index> forces a tile
@@ -517,7 +592,9 @@ enum class XTile { T120 = 0, T120x96, T128x72, T160x72, T128, COUNT };
 static XTile choose_xtile(int P2, int pp) {
     if (const char* f = std::getenv("MG_XTILE")) {
         const int i = std::atoi(f);
-        if (i >= 0 && i < (int)XTile::COUNT) return (XTile)i;
+        if (i >= 0 && i < (int)XTile::COUNT &&
+            ((XTile)i != XTile::T120x128NS || nsplit_efficiency(P2, pp) > 0.0))
+            return (XTile)i;
     }
     struct Cand { XTile t; int bm, bn; double pipe; };
     const Cand cands[] = {{XTile::T120, 120, 120, 15.0 / 16.0},
@@ -532,6 +609,7 @@ static XTile choose_xtile(int P2, int pp) {
                          ((double)ceil_div(P2, c.bm) * c.bm * ceil_div(pp, c.bn) * c.bn);
         if (e > be + 1e-9) { be = e; best = c.t; }
     }
+    if (nsplit_efficiency(P2, pp) > be + 1e-9) best = XTile::T120x128NS;
     return best;
 }
 
@@ -547,6 +625,13 @@ static void attr_x() {
     MG_CUDA(cudaFuncSetAttribute(k_x_contract_p<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)XPipeP<Cfg>::smem_bytes));
 }
+template <class Cfg>
+static void launch_x_ns(int num_sms, cudaStream_t st, const double* S, const double* H, int nrows,
+                        int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* G,
+                        const MgBounds& bd) {
+    k_x_contract_ns<Cfg><<<num_sms, XPipeNS<Cfg>::THREADS, XPipeNS<Cfg>::smem_bytes, st>>>(
+        S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd);
+}
 static void launch_xtile(XTile xt, int num_sms, cudaStream_t st, const double* S, const double* H,
                          int nrows, int row_b1, int row_b3, int p, int P2, int Nx, int NxP,
                          double* G, const MgBounds& bd) {
@@ -555,6 +640,7 @@ static void launch_xtile(XTile xt, int num_sms, cudaStream_t st, const double* S
         case XTile::T120x96: launch_x<CfgX120x96>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
         case XTile::T128x72: launch_x<CfgX128x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
         case XTile::T160x72: launch_x<CfgX160x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
+        case XTile::T120x128NS: launch_x_ns<CfgX120x128>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
         default: launch_x<CfgX128>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
     }
 }
@@ -1087,6 +1173,9 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         attr_x<CfgX128x72>();
         attr_x<CfgX160x72>();
         attr_x<CfgX128>();
+        MG_CUDA(cudaFuncSetAttribute(k_x_contract_ns<CfgX120x128>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)XPipeNS<CfgX120x128>::smem_bytes));
         MG_CUDA(cudaFuncSetAttribute(k_pair_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_run));
         attr_done = true;
