@@ -255,15 +255,20 @@ def slab_triples(l_min, l_max, l2_begin, l2_end):
 
 
 def _sweep_job(args):
-    (begin, end, q, qt, C, v, wr2, entries, l_min, l_max, block, h2_mode) = args
+    begin, end, l_min, l_max, block, h2_mode = args
+    d = _SHARED
     l1, l2, l3 = domain_triples(l_min, l_max, begin, end)
-    return sweep_triples(q, qt, C, v, wr2, entries, l_min, l1, l2, l3, block, h2_mode)
+    return sweep_triples(d["q"], d["qt"], d["C"], d["v"], d["wr2"], d["entries"], l_min, l1, l2,
+                         l3, block, h2_mode)
 
 
 def gamma3d(q, qt, C, v, wr2, entries, l_min, l_max, begin=0, end=None, workers=1,
             block=64, h2_mode="gosper") -> np.ndarray:
     """gamma3d_matrix (engine3d.py:156-186): make_plan over [begin, end), fork pool of
-    _sweep_chunk, merge in worker order (scheduler.py:32-66)."""
+    _sweep_chunk, merge in worker order (scheduler.py:32-66).  Same split, same order as the
+    reference; the tables reach the workers through fork instead of being pickled per job
+    (the reference pickles them once per Γ, which is noise at its run times but would
+    dominate the bounded samples timed here)."""
     if end is None:
         end = domain_count(l_min, l_max)
     total = end - begin
@@ -271,13 +276,17 @@ def gamma3d(q, qt, C, v, wr2, entries, l_min, l_max, begin=0, end=None, workers=
     jobs, s = [], begin
     for w in range(workers):
         size = base + (1 if w < extra else 0)
-        jobs.append((s, s + size, q, qt, C, v, wr2, entries, l_min, l_max, block, h2_mode))
+        jobs.append((s, s + size, l_min, l_max, block, h2_mode))
         s += size
-    if workers == 1:
-        parts = [_sweep_job(jobs[0])]
-    else:
-        with get_context("fork").Pool(workers) as pool:
-            parts = pool.map(_sweep_job, jobs)
+    _SHARED.update(q=q, qt=qt, C=C, v=v, wr2=wr2, entries=entries)
+    try:
+        if workers == 1:
+            parts = [_sweep_job(jobs[0])]
+        else:
+            with get_context("fork").Pool(workers) as pool:
+                parts = pool.map(_sweep_job, jobs)
+    finally:
+        _SHARED.clear()
     out = parts[0].copy()
     for p in parts[1:]:
         out += p

@@ -1757,9 +1757,75 @@ template <int PP>
 __host__ __device__ constexpr int ns_gi0(int k) {
     return k < (PP / 2) * (PP / 4) ? (k % (PP / 4)) * 4 : (k - (PP / 2) * (PP / 4)) * 4;
 }
+// The K order as a "design": R registers per lane and table, k-step k multiplies registers
+// (I(k), J(k)) — the same in every lane — and lane t4's register i holds component
+// comp(t4, i), so k-slot t4 of k-step k is the pair (comp(t4, I), comp(t4, J)).  A design is
+// valid when the 4 x NK (lane, k-step) pairs cover every unordered pair once (padding slots
+// get Ã = 0).  In a chunk block, component c lives in row row(c), its 8 columns rotated by 4 h(c)
+// (the swizzle that keeps the per-lane-component LDS.64 bank-conflict free: the components a
+// register takes across the four lanes of a quad must fall in different 32-byte quarters of
+// the 128-byte bank window, quarter = 2 (row & 1) + (h ^ (column >= 4))).
+//   NsRot<PP>   the rotation design above: R = PP registers.
+//   NsSix       PP = 8 on R = 6 registers (found by exhaustive search, tools/ns_design.py):
+//               shared-memory read traffic is 4 lanes x R x 2 tables per column, so 6
+//               registers read 3 KB per 8-column chunk instead of 4 KB.  The kernel was
+//               co-limited by the shared-memory pipe (44 wavefronts per chunk-warp against
+//               180 FP64-datapath cycles on four sub-partitions).
+template <int PP>
+struct NsRot {
+    static constexpr int R = PP, NK = ns_groups<PP>();
+    __host__ __device__ static constexpr int I(int k) { return ns_gi0<PP>(k); }
+    __host__ __device__ static constexpr int J(int k) { return (ns_gi0<PP>(k) + ns_gd<PP>(k)) % PP; }
+    __host__ __device__ static constexpr int comp(int t4, int i) { return (i + t4) % PP; }
+    __host__ __device__ static constexpr bool live(int k, int t4) {
+        return 2 * ns_gd<PP>(k) < PP || ns_gi0<PP>(k) + t4 < PP / 2;
+    }
+    __host__ __device__ static constexpr int row(int c) { return c; }
+    __host__ __device__ static constexpr int h(int c) { return (c >> 1) & 1; }
+};
+struct NsSix {
+    static constexpr int R = 6, NK = 9;
+    __host__ __device__ static constexpr int I(int k) {
+        constexpr int t[9] = {0, 1, 0, 0, 0, 0, 0, 1, 1};
+        return t[k];
+    }
+    __host__ __device__ static constexpr int J(int k) {
+        constexpr int t[9] = {0, 1, 1, 2, 3, 4, 5, 2, 3};
+        return t[k];
+    }
+    __host__ __device__ static constexpr int comp(int t4, int i) {
+        constexpr int t[4][6] = {{0, 1, 2, 3, 4, 5}, {6, 2, 4, 7, 0, 1}, {7, 4, 1, 3, 0, 5},
+                                 {5, 3, 2, 6, 1, 4}};
+        return t[t4][i];
+    }
+    __host__ __device__ static constexpr bool live(int, int) { return true; }
+    // quarter labels (0,1,0,2,3,2,1,3): even rows <- components 0,1,2,6; odd rows <- 3,4,5,7
+    __host__ __device__ static constexpr int row(int c) {
+        constexpr int t[8] = {0, 2, 4, 1, 3, 5, 6, 7};
+        return t[c];
+    }
+    __host__ __device__ static constexpr int h(int c) {
+        constexpr int t[8] = {0, 1, 0, 0, 1, 0, 1, 1};
+        return t[c];
+    }
+};
+#ifndef NS_ROT8
+#define NS_ROT8 0  // 1: rotation design at PP = 8 too (A/B measurements)
+#endif
+template <int PP> struct NsDesignOf { using type = NsRot<PP>; };
+#if !NS_ROT8
+template <> struct NsDesignOf<8> { using type = NsSix; };
+#endif
+template <int PP> using NsDesign = typename NsDesignOf<PP>::type;
+// slot (doubles) of (component c, column xi) inside a PP x 8 chunk block
+template <int PP>
+__host__ __device__ inline int ns_slot(int c, int xi) {
+    return NsDesign<PP>::row(c) * 8 + ((xi + 4 * NsDesign<PP>::h(c)) & 7);
+}
+
 template <int PP>
 struct NsAfrag {
-    double a[ns_groups<PP>()][32];  // [k-step][lane]: lane (g, t4) holds Ã[g][pair(k, t4)]
+    double a[NsDesign<PP>::NK][32];  // [k-step][lane]: lane (g, t4) holds Ã[g][pair(k, t4)]
 };
 
 // Tables of the DMMA kernel, x in blocks of 8 columns ("chunks"), one 8-column row per
@@ -1770,8 +1836,9 @@ struct NsAfrag {
 //                     land on opposite column halves of the 128-byte bank window);
 //   Q1W[l][xb][c][8]: wr2[x] q̃[c][x][l] (no swizzle: read as double2 per lane).
 // Components >= p and columns >= Nx are zero.  Built from the plan's QT[l][c][NxP].
+template <int PP>
 __global__ void k_ns_tables(const double* __restrict__ QT, const double* __restrict__ wr2, int p,
-                            int PP, int Nx, int NxP, int L, int XB8, double* __restrict__ QTS,
+                            int Nx, int NxP, int L, int XB8, double* __restrict__ QTS,
                             double* __restrict__ Q1W) {
     const int64_t total = (int64_t)L * XB8 * PP * 8;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -1785,7 +1852,7 @@ __global__ void k_ns_tables(const double* __restrict__ QT, const double* __restr
         const int x = xb * 8 + xi;
         const double val = (c < p && x < Nx) ? QT[((int64_t)l * p + c) * NxP + x] : 0.0;
         Q1W[i] = x < Nx ? wr2[x] * val : 0.0;
-        QTS[(i & ~(int64_t)7) + ((xi + 4 * ((c >> 1) & 1)) & 7)] = val;
+        QTS[(i / (PP * 8)) * (PP * 8) + ns_slot<PP>(c, xi)] = val;
     }
 }
 
@@ -1839,7 +1906,8 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
               const NsAfrag<PP> af, const double* __restrict__ q, const int* __restrict__ modes,
               int P, int nm, int L, int l_min, double* __restrict__ partial, MgBounds bd) {
     using SG = NsStage<PP>;
-    constexpr int NK = ns_groups<PP>(), CH = NS_CH, NST = NS_ST, CHUNK = SG::CHUNK;
+    using DS = NsDesign<PP>;
+    constexpr int NK = DS::NK, NR = DS::R, CH = NS_CH, NST = NS_ST, CHUNK = SG::CHUNK;
     constexpr int NW = NSD_THREADS / 32;
     extern __shared__ __align__(16) double sh[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1861,12 +1929,9 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
     for (int k = 0; k < NK; ++k) a[k] = af.a[k][lane];
     // lane's rotated component offsets (doubles) within a chunk block: register i holds
     // component (i + t4) mod PP of column g, stored at swizzled column position
-    int off[PP];
+    int off[NR];
 #pragma unroll
-    for (int i = 0; i < PP; ++i) {
-        const int c = (i + t4) % PP;
-        off[i] = c * 8 + ((g + 4 * ((c >> 1) & 1)) & 7);
-    }
+    for (int i = 0; i < NR; ++i) off[i] = ns_slot<PP>(DS::comp(t4, i), g);
     __syncthreads();
     double* my = bacc + (size_t)warp * nm;
     const int64_t nwarps = (int64_t)gridDim.x * NW;
@@ -1923,15 +1988,15 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
                 if (u < nch) {
                     const double* b2 = st + u * CHUNK;
                     const double* b3 = st + (CH + u) * CHUNK;
-                    double r2[PP], r3[PP];
+                    double r2[NR], r3[NR];
 #pragma unroll
-                    for (int i = 0; i < PP; ++i) {
+                    for (int i = 0; i < NR; ++i) {
                         r2[i] = b2[off[i]];
                         r3[i] = b3[off[i]];
                     }
 #pragma unroll
                     for (int k = 0; k < NK; ++k) {
-                        const int i0 = ns_gi0<PP>(k), j = (ns_gi0<PP>(k) + ns_gd<PP>(k)) % PP;
+                        const int i0 = DS::I(k), j = DS::J(k);
                         S[u][k] = r2[i0] * r3[j] + r2[j] * r3[i0];
                     }
                 } else {
@@ -1984,11 +2049,12 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
 template <int PP>
 static NsAfrag<PP> ns_afrag(const std::vector<double>& at, int p, int P2) {
     NsAfrag<PP> f;
-    for (int k = 0; k < ns_groups<PP>(); ++k)
+    using DS = NsDesign<PP>;
+    for (int k = 0; k < DS::NK; ++k)
         for (int lane = 0; lane < 32; ++lane) {
-            const int g = lane >> 2, t4 = lane & 3, d = ns_gd<PP>(k), r = ns_gi0<PP>(k) + t4;
-            const int a = r % PP, b = (r + d) % PP;
-            const bool ok = (2 * d < PP || r < PP / 2) && a < p && b < p && g < p;
+            const int g = lane >> 2, t4 = lane & 3;
+            const int a = DS::comp(t4, DS::I(k)), b = DS::comp(t4, DS::J(k));
+            const bool ok = DS::live(k, t4) && a < p && b < p && g < p;
             f.a[k][lane] = ok ? at[(size_t)g * P2 + pair_idx(std::min(a, b), std::max(a, b))] : 0.0;
         }
     return f;
@@ -2000,8 +2066,8 @@ static void launch_nonsep_dmma(mg_plan* Pl, const std::vector<double>& at, cudaS
     if (!Pl->ns_qt2.p) {  // x-chunked, swizzled q̃ tables (once per plan)
         Pl->ns_qt2.alloc((size_t)Pl->L * XB8 * PP * 8);
         Pl->ns_q1w.alloc((size_t)Pl->L * XB8 * PP * 8);
-        k_ns_tables<<<1184, 256, 0, st>>>(Pl->QT.p, Pl->wr2.p, Pl->p, PP, Pl->Nx, Pl->NxP, Pl->L,
-                                          XB8, Pl->ns_qt2.p, Pl->ns_q1w.p);
+        k_ns_tables<PP><<<1184, 256, 0, st>>>(Pl->QT.p, Pl->wr2.p, Pl->p, Pl->Nx, Pl->NxP, Pl->L,
+                                              XB8, Pl->ns_qt2.p, Pl->ns_q1w.p);
         MG_LAUNCHED();
     }
     const NsAfrag<PP> af = ns_afrag<PP>(at, Pl->p, Pl->P2);

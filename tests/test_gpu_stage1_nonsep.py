@@ -63,9 +63,12 @@ class TestStage1:
         d = qtilde_ref.delta_table(hi.k, hi.eps, 2, hi.l_max)
         Cr = qtilde_ref.c_ell(d, hi.k, hi.wk)
         assert np.max(np.abs(C / Cr - 1)) < 1e-11
-        ref = qtilde_ref.qtilde(hi.k, hi.wk, hi.x, hi.qk, d, 2, hi.l_max, ells)
+        # the scipy oracle costs ~2 µs per (l, k, x): compare on ~125 evenly spaced x (both ends
+        # included) so the whole GPU suite stays well inside the driver's 20-minute limit
+        xi = np.unique(np.linspace(0, hi.x.size - 1, 125).round().astype(int))
+        ref = qtilde_ref.qtilde(hi.k, hi.wk, hi.x[xi], hi.qk, d, 2, hi.l_max, ells)
         for l in ells:
-            a, b = qt[:, :, l - 2], ref[:, :, l - 2]
+            a, b = qt[:, xi, l - 2], ref[:, :, l - 2]
             assert np.linalg.norm(a - b) <= 1e-11 * np.linalg.norm(b), l
 
     def test_gamma_end_to_end_c0(self, g_c0):
