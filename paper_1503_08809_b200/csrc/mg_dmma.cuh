@@ -483,13 +483,13 @@ struct PipeTMAPersistent {
 // N-split form of the persistent pipeline, for tiles whose last N tile is mostly padding
 // (p = 15 x contraction: N = 225 = 128 + 97).  The item's valid n-fragments nfr (of
 // FN * WARPS_N) are dealt to the WARPS_N warp columns as evenly as possible, so a warp owns
-// FN or FN - 1 n-fragments (one warp-uniform dispatch per item into two compiled loop bodies:
-// no per-DMMA predicates) starting at a per-item column offset.  Warp columns are rotated by
+// FN, FN - 1 or FN - 2 n-fragments (one warp-uniform dispatch per item into separately
+// compiled loop bodies: no per-DMMA predicates) starting at a per-item column offset.  Warp columns are rotated by
 // the warp row (wn = (warp + warp / WARPS_N) % WARPS_N), so the warps with the extra fragment
 // fall on different SM sub-partitions (warp % 4) and the four DMMA units stay balanced:
 // 13 n-fragments run as 4,3,3,3 -> 50 fragment-steps per sub-partition instead of 60.
 // Extra producer contract: int nfrags(int it) (valid n-fragments of the item, each warp
-// column must get FN or FN - 1); the epilogue is epi(it, acc, wm, wn, nf).
+// column must get FN - 2 .. FN and at least 1); the epilogue is epi(it, acc, wm, wn, nf).
 template <class Cfg, int BK, int STAGES, bool AK, bool BKM>
 struct PipeTMAPersistentNS {
     using Base = PipeTMA<Cfg, BK, STAGES, AK, BKM>;
@@ -608,8 +608,11 @@ struct PipeTMAPersistentNS {
             const int wn = 8 * (wni * base + min(wni, rem));
             if (nf == FN)
                 item_loop<FN>(prod, smem, full, empty, kts, kvl, wm, wn, g, acc);
-            else
+            else if (FN < 3 || nf == FN - 1)
                 item_loop<FN - 1>(prod, smem, full, empty, kts, kvl, wm, wn, g, acc);
+            else
+                item_loop<(FN >= 3 ? FN - 2 : 1)>(prod, smem, full, empty, kts, kvl, wm, wn, g,
+                                                  acc);
             epi(it, acc, wm, wn, nf);
         }
     }

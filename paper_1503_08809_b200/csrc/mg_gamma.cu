@@ -561,27 +561,27 @@ using CfgX128 = TileCfg<2, 4, 8, 4>;
 //                                                            p = 15: 225 = 16 + 13 n-fragments
 using CfgX120x128 = TileCfg<3, 4, 5, 4>;
 
-enum class XTile { T120 = 0, T120x96, T128x72, T160x72, T128, T120x128NS, COUNT };
+enum class XTile { T120 = 0, T120x96, T128x72, T160x72, T128, T120x128NS, T128x72NS, T160x72NS,
+                   COUNT };
 
-// DMMA-pipe model of the N-split tile: fragment-steps of the busiest SM sub-partition per row
-// (sub-partition s = warp % 4 holds warp rows 0..2 with warp columns s, s+1, s+2 mod 4) against
-// the useful ones; 0 when a warp column would get fewer than FN - 1 fragments.
+// DMMA-pipe model of an N-split tile: fragment-steps of the busiest SM sub-partition per row
+// (sub-partition = warp % 4; warp w sits in warp row w / WARPS_N and warp column
+// (w + w / WARPS_N) % WARPS_N) against the useful ones; 0 when a warp column of the partial N
+// tile would get fewer than max(1, FN - 2) fragments.
+template <class C>
 static double nsplit_efficiency(int P2, int pp) {
-    using C = CfgX120x128;
     const int MT = ceil_div(P2, C::BM), NT = ceil_div(pp, C::BN);
     double cost = 0.0;
     for (int nt = 0; nt < NT; ++nt) {
         const int nfr = (std::min(C::BN, pp - nt * C::BN) + 7) / 8;
         const int base = nfr / C::WARPS_N, rem = nfr % C::WARPS_N;
-        if (base + (rem ? 1 : 0) > C::FN || base < C::FN - 1) return 0.0;
-        int worst = 0;
-        for (int s = 0; s < 4; ++s) {
-            int load = 0;
-            for (int wmi = 0; wmi < C::WARPS_M; ++wmi)
-                load += C::FM * (base + (((s + wmi) % C::WARPS_N) < rem ? 1 : 0));
-            worst = std::max(worst, load);
+        if (base < std::max(1, C::FN - 2)) return 0.0;
+        int load[4] = {0, 0, 0, 0};
+        for (int w = 0; w < C::WARPS_M * C::WARPS_N; ++w) {
+            const int wni = (w + w / C::WARPS_N) % C::WARPS_N;
+            load[w % 4] += C::FM * (base + (wni < rem ? 1 : 0));
         }
-        cost += worst;
+        cost += *std::max_element(load, load + 4);
     }
     return ((double)P2 * pp / 64.0 / 4.0) / (cost * MT);
 }
@@ -590,10 +590,13 @@ static double nsplit_efficiency(int P2, int pp) {
 // (sub-partition balance / measured DMMA-pipe utilisation).  MG_XTILE=<index> forces a tile
 // (A/B measurements).
 static XTile choose_xtile(int P2, int pp) {
+    const double ens[3] = {nsplit_efficiency<CfgX120x128>(P2, pp),
+                           nsplit_efficiency<CfgX128x72>(P2, pp),
+                           nsplit_efficiency<CfgX160x72>(P2, pp)};
     if (const char* f = std::getenv("MG_XTILE")) {
         const int i = std::atoi(f);
         if (i >= 0 && i < (int)XTile::COUNT &&
-            ((XTile)i != XTile::T120x128NS || nsplit_efficiency(P2, pp) > 0.0))
+            (i < (int)XTile::T120x128NS || ens[i - (int)XTile::T120x128NS] > 0.0))
             return (XTile)i;
     }
     struct Cand { XTile t; int bm, bn; double pipe; };
@@ -609,7 +612,9 @@ static XTile choose_xtile(int P2, int pp) {
                          ((double)ceil_div(P2, c.bm) * c.bm * ceil_div(pp, c.bn) * c.bn);
         if (e > be + 1e-9) { be = e; best = c.t; }
     }
-    if (nsplit_efficiency(P2, pp) > be + 1e-9) best = XTile::T120x128NS;
+    // N-split forms (same tiles, partial last N tile dealt over the warp columns)
+    for (int i = 0; i < 3; ++i)
+        if (ens[i] > be + 1e-9) { be = ens[i]; best = (XTile)((int)XTile::T120x128NS + i); }
     return best;
 }
 
@@ -632,6 +637,11 @@ static void launch_x_ns(int num_sms, cudaStream_t st, const double* S, const dou
     k_x_contract_ns<Cfg><<<num_sms, XPipeNS<Cfg>::THREADS, XPipeNS<Cfg>::smem_bytes, st>>>(
         S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd);
 }
+template <class Cfg>
+static void attr_x_ns() {
+    MG_CUDA(cudaFuncSetAttribute(k_x_contract_ns<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)XPipeNS<Cfg>::smem_bytes));
+}
 static void launch_xtile(XTile xt, int num_sms, cudaStream_t st, const double* S, const double* H,
                          int nrows, int row_b1, int row_b3, int p, int P2, int Nx, int NxP,
                          double* G, const MgBounds& bd) {
@@ -641,6 +651,8 @@ static void launch_xtile(XTile xt, int num_sms, cudaStream_t st, const double* S
         case XTile::T128x72: launch_x<CfgX128x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
         case XTile::T160x72: launch_x<CfgX160x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
         case XTile::T120x128NS: launch_x_ns<CfgX120x128>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
+        case XTile::T128x72NS: launch_x_ns<CfgX128x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
+        case XTile::T160x72NS: launch_x_ns<CfgX160x72>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
         default: launch_x<CfgX128>(num_sms, st, S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd); break;
     }
 }
@@ -1173,9 +1185,9 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         attr_x<CfgX128x72>();
         attr_x<CfgX160x72>();
         attr_x<CfgX128>();
-        MG_CUDA(cudaFuncSetAttribute(k_x_contract_ns<CfgX120x128>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)XPipeNS<CfgX120x128>::smem_bytes));
+        attr_x_ns<CfgX120x128>();
+        attr_x_ns<CfgX128x72>();
+        attr_x_ns<CfgX160x72>();
         MG_CUDA(cudaFuncSetAttribute(k_pair_contract, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_run));
         attr_done = true;
@@ -1875,21 +1887,37 @@ __global__ void k_ns_weights(const int4* __restrict__ trip, const double* __rest
 // its triples' data into shared memory with cp.async.bulk (TMA engine, no LSU wavefronts),
 // NS_ST stages of NS_CH chunks: [l2 chunks][l3 chunks], completing on a per-warp, per-stage
 // mbarrier; the rotated reads are then LDS.64 (2 wavefronts each).  The wr2-weighted l1 row
-// (one double2 per lane per chunk, no redundancy) is read from global memory.  12 warps per
-// CTA (3 per SM sub-partition) with NS_CH = 4 accumulator chains each: a single chain is
-// latency-bound, the sub-partition's DMMA pipe needs several in flight.
+// (one double2 per lane per chunk, no redundancy) is read from global memory.
 // Lane 0 of the warp is the producer: after the warp has consumed a stage it refills the slot
 // with the stage NS_ST ahead (crossing into the warp's next triple), so copies run under the
 // DMMAs of the stages in between.
+// Warps and chains (measured, profiles/r02_nonsep_dmma_variants.txt): a warp that has issued
+// a DMMA cannot issue anything for ~14 cycles, so its ~300 non-tensor instructions per stage
+// (LDS, pair products, refill, loop) never overlap its own tensor work — only other warps'.
+// With w warps per SM sub-partition each on the FP64 datapath a fraction d ~ 1/3 of its time,
+// the datapath is busy ~1 - (1 - d)^w: 12 warps per CTA (w = 3) reach 69 %, 16 warps 75 %,
+// where it levels off (20 and 24 warps: same).  16 warps leave 128 registers per lane, so the
+// pair products of only NS_G = 2 chunks are live at once (2 accumulator chains per warp; the
+// other warps of the sub-partition cover the DMMA D -> C latency), in NS_CH / NS_G groups per
+// stage, and 2 stages of 4 KB per warp keep the CTA at 128 KB of shared memory.
 #ifndef NSD_THREADS_
-#define NSD_THREADS_ 384
+#define NSD_THREADS_ 512
 #endif
 constexpr int NSD_THREADS = NSD_THREADS_;
 #ifndef NS_CH
 #define NS_CH 4  // chunks of 8 x columns per stage
 #endif
 #ifndef NS_ST
-#define NS_ST 3  // stages per warp
+#define NS_ST 2  // stages per warp
+#endif
+#ifndef NS_FENCE
+#define NS_FENCE 0  // 1: generic->async proxy fence before a slot's refill (A/B measurements)
+#endif
+#ifndef NS_ASMEM
+#define NS_ASMEM 0  // 1: Ã fragments read from shared memory per k-step (more warps per CTA)
+#endif
+#ifndef NS_G
+#define NS_G 2  // chunks whose pair products are live at once (accumulator chains in flight)
 #endif
 
 template <int PP>
@@ -1924,9 +1952,23 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
         for (int s = 0; s < NST; ++s) mbar_init(full + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
+    // Ã fragments: registers for the whole kernel.  The empty asm makes each value opaque, so
+    // under register pressure ptxas spills it instead of re-reading the kernel parameter with a
+    // per-lane index (LDC with 32 different addresses serialises: measured 6.7 -> 17.5 ms).
+#if NS_ASMEM
+    // Ã fragments in shared memory instead (one conflict-free LDS.64 per k-step and group):
+    // frees 2 NK registers per lane for CTAs of more than 16 warps (96-register cap)
+    double* a_s = reinterpret_cast<double*>(md + 3 * nm + (nm & 1));
+    for (int i = tid; i < NK * 32; i += NSD_THREADS) a_s[i] = af.a[i >> 5][i & 31];
+    a_s += lane;
+#else
     double a[NK];
 #pragma unroll
-    for (int k = 0; k < NK; ++k) a[k] = af.a[k][lane];
+    for (int k = 0; k < NK; ++k) {
+        a[k] = af.a[k][lane];
+        asm volatile("" : "+d"(a[k]));
+    }
+#endif
     // lane's rotated component offsets (doubles) within a chunk block: register i holds
     // component (i + t4) mod PP of column g, stored at swizzled column position
     int off[NR];
@@ -1938,34 +1980,125 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
     const int nstg = (XB8 + CH - 1) / CH;  // stages per triple
     const int64_t lstride = (int64_t)XB8 * CHUNK;
 
-    // producer cursor (lane 0): the (triple, stage) to issue next
+    // producer cursor (lane 0): the (triple, stage) to issue next and its source rows
     int64_t pt = (int64_t)blockIdx.x * NW + warp;
     int ps = 0;
-    int4 ptr = pt < count ? trip[pt] : make_int4(0, 0, 0, 0);
+    const double *src2 = QTS, *src3 = QTS;
+    auto load_cursor = [&]() {
+        const int4 ptr = trip[pt];
+        MG_DCHECK(ptr.x >= l_min && ptr.y >= ptr.x && ptr.z >= ptr.y && ptr.z - l_min < L, CK_NS_L);
+        src2 = QTS + (ptr.y - l_min) * lstride;
+        src3 = QTS + (ptr.z - l_min) * lstride;
+    };
+    if (pt < count) load_cursor();
     auto issue = [&](int slot) {
         if (pt >= count) return;
-        const int c0 = ps * CH, nch = min(CH, XB8 - c0);
+        const int nch = min(CH, XB8 - ps * CH);
         const uint32_t bytes = (uint32_t)nch * CHUNK * 8;
         double* st = stg + (size_t)slot * SG::DOUBLES;
-        MG_DCHECK(ptr.x >= l_min && ptr.y >= ptr.x && ptr.z >= ptr.y && ptr.z - l_min < L, CK_NS_L);
-        MG_DCHECK(in_range((ptr.y - l_min) * lstride + (int64_t)c0 * CHUNK, (int64_t)nch * CHUNK,
-                           bd.qts) &&
-                      in_range((ptr.z - l_min) * lstride + (int64_t)c0 * CHUNK,
-                               (int64_t)nch * CHUNK, bd.qts),
+        MG_DCHECK(in_range(src2 - QTS, (int64_t)nch * CHUNK, bd.qts) &&
+                      in_range(src3 - QTS, (int64_t)nch * CHUNK, bd.qts),
                   CK_NS_QTS);
         mbar_arrive_expect_tx(full + slot, 2 * bytes);
-        bulk_g2s(st, QTS + (ptr.y - l_min) * lstride + (int64_t)c0 * CHUNK, bytes, full + slot);
-        bulk_g2s(st + CH * CHUNK, QTS + (ptr.z - l_min) * lstride + (int64_t)c0 * CHUNK, bytes,
-                 full + slot);
+        bulk_g2s(st, src2, bytes, full + slot);
+        bulk_g2s(st + CH * CHUNK, src3, bytes, full + slot);
+        src2 += CH * CHUNK;
+        src3 += CH * CHUNK;
         if (++ps == nstg) {
             ps = 0;
             pt += nwarps;
-            if (pt < count) ptr = trip[pt];
+            if (pt < count) load_cursor();
         }
     };
     if (lane == 0)
         for (int s = 0; s < NST; ++s) issue(s);
     __syncwarp();
+
+    // One stage = NS_CH chunks: their pair products S first (each chunk's rotated q̃ rows are
+    // dead once its NK S values exist), then the DMMAs of the NS_CH independent accumulator
+    // chains (a warp keeps several DMMAs in flight; the DMMA D -> C latency is ~4 issue slots
+    // of the sub-partition's DMMA pipe), then the l1 contraction.  FULL: all NS_CH chunks hold
+    // data (straight-line code, no zero fill); otherwise chunks >= nch are skipped, DMMAs
+    // included (the last stage of a triple: 38 chunks = 9 x 4 + 2 at Nx = 300).
+    // One group of NS_G chunks: pair products, DMMA chains, l1 contraction.  FULL: every chunk
+    // of the group holds data (straight-line code); otherwise chunks >= nv are skipped.
+    auto group_body = [&](auto full_c, const double* st, const double* b1, int u0, int nv,
+                          double& xs0, double& xs1) {
+        constexpr bool FULL = decltype(full_c)::value;
+        constexpr int G = NS_G;
+        double S[G][NK];
+#pragma unroll
+        for (int v = 0; v < G; ++v) {
+            if (FULL || v < nv) {
+                const double* b2 = st + (u0 + v) * CHUNK;
+                const double* b3 = st + (CH + u0 + v) * CHUNK;
+                double r2[NR], r3[NR];
+#pragma unroll
+                for (int i = 0; i < NR; ++i) {
+                    r2[i] = b2[off[i]];
+                    r3[i] = b3[off[i]];
+                }
+#pragma unroll
+                for (int k = 0; k < NK; ++k) {
+                    const int i0 = DS::I(k), j = DS::J(k);
+                    S[v][k] = r2[i0] * r3[j] + r2[j] * r3[i0];
+                }
+            }
+        }
+        // accumulator row c = g exists only for g < PP (PP = 4: lanes g >= 4 hold zero rows of
+        // T and must not read past their chunk's PP component rows)
+        double2 w[G];
+#pragma unroll
+        for (int v = 0; v < G; ++v) {
+            MG_DCHECK(!((FULL || v < nv) && g < PP) ||
+                          in_range(b1 + (u0 + v) * CHUNK - Q1W, 2, bd.q1w), CK_NS_Q1W);
+            w[v] = ((FULL || v < nv) && g < PP)
+                       ? __ldg(reinterpret_cast<const double2*>(b1 + (u0 + v) * CHUNK))
+                       : make_double2(0.0, 0.0);
+        }
+        double acc[G][2];
+#pragma unroll
+        for (int v = 0; v < G; ++v) acc[v][0] = acc[v][1] = 0.0;
+#pragma unroll
+        for (int k = 0; k < NK; ++k)
+#if NS_ASMEM
+            {
+                const double ak = a_s[k * 32];
+#pragma unroll
+                for (int v = 0; v < G; ++v)
+                    if (FULL || v < nv) dmma884(acc[v], ak, S[v][k]);
+            }
+#else
+#pragma unroll
+            for (int v = 0; v < G; ++v)
+                if (FULL || v < nv) dmma884(acc[v], a[k], S[v][k]);
+#endif
+#pragma unroll
+        for (int v = 0; v < G; ++v) {
+            xs0 = fma(w[v].x, acc[v][0], xs0);
+            xs1 = fma(w[v].y, acc[v][1], xs1);
+        }
+    };
+    // One stage = NS_CH chunks in groups of NS_G (NS_G chains in flight, NS_G x NK pair products
+    // live).  A stage whose chunks all hold data is one straight-line block; the last stage of
+    // a triple (38 chunks = 9 x 4 + 2 at Nx = 300) runs its full groups, then the remainder.
+    auto stage_body = [&](const double* st, const double* b1, int nch, double& xs0, double& xs1) {
+        constexpr int G = NS_G;
+        static_assert(CH % G == 0, "chunk groups must divide the stage");
+        if (nch == CH) {
+#pragma unroll
+            for (int u0 = 0; u0 < CH; u0 += G)
+                group_body(std::true_type{}, st, b1, u0, G, xs0, xs1);
+        } else {
+#pragma unroll
+            for (int u0 = 0; u0 < CH; u0 += G) {
+                if (u0 + G <= nch)
+                    group_body(std::true_type{}, st, b1, u0, G, xs0, xs1);
+                else if (u0 < nch)
+                    group_body(std::false_type{}, st, b1, u0, nch - u0, xs0, xs1);
+            }
+        }
+    };
 
     uint32_t gst = 0;  // stages consumed by this warp (slot = gst % NST, phase = gst / NST)
     for (int64_t t = (int64_t)blockIdx.x * NW + warp; t < count; t += nwarps) {
@@ -1977,57 +2110,16 @@ k_nonsep_dmma(const int4* __restrict__ trip, const double* __restrict__ WZ, int6
             mbar_wait(full + slot, (int)((gst / NST) & 1));
             const double* st = stg + (size_t)slot * SG::DOUBLES;
             const int nch = min(CH, XB8 - s * CH);
-            // All NS_CH chunks of the stage at once: their pair products S first (each chunk's
-            // rotated q̃ rows are dead once its 9 S values exist), then the DMMAs of the
-            // NS_CH independent accumulator chains interleaved k-step by k-step, so a warp
-            // keeps NS_CH DMMAs in flight (the DMMA D -> C latency is ~4 issue slots of the
-            // sub-partition's DMMA pipe).
-            double S[CH][NK];
-#pragma unroll
-            for (int u = 0; u < CH; ++u) {
-                if (u < nch) {
-                    const double* b2 = st + u * CHUNK;
-                    const double* b3 = st + (CH + u) * CHUNK;
-                    double r2[NR], r3[NR];
-#pragma unroll
-                    for (int i = 0; i < NR; ++i) {
-                        r2[i] = b2[off[i]];
-                        r3[i] = b3[off[i]];
-                    }
-#pragma unroll
-                    for (int k = 0; k < NK; ++k) {
-                        const int i0 = DS::I(k), j = DS::J(k);
-                        S[u][k] = r2[i0] * r3[j] + r2[j] * r3[i0];
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < NK; ++k) S[u][k] = 0.0;
-                }
-            }
-            double acc[CH][2];
-#pragma unroll
-            for (int u = 0; u < CH; ++u) acc[u][0] = acc[u][1] = 0.0;
-#pragma unroll
-            for (int k = 0; k < NK; ++k)
-#pragma unroll
-                for (int u = 0; u < CH; ++u) dmma884(acc[u], a[k], S[u][k]);
-            // accumulator row c = g exists only for g < PP (PP = 4: lanes g >= 4 hold zero
-            // rows of T and must not read past their chunk's PP component rows)
             const double* b1 = p1 + (int64_t)s * CH * CHUNK;
-#pragma unroll
-            for (int u = 0; u < CH; ++u) {
-                MG_DCHECK(!(u < nch && g < PP) || in_range(b1 + u * CHUNK - Q1W, 2, bd.q1w),
-                          CK_NS_Q1W);
-                const double2 w = (u < nch && g < PP)
-                                      ? __ldg(reinterpret_cast<const double2*>(b1 + u * CHUNK))
-                                      : make_double2(0.0, 0.0);
-                xs0 = fma(w.x, acc[u][0], xs0);
-                xs1 = fma(w.y, acc[u][1], xs1);
-            }
-            // slot consumed by every lane: refill it with the stage NST ahead
+            stage_body(st, b1, nch, xs0, xs1);
+            // Slot consumed by every lane (its LDS results have been used by the FP64 ops
+            // above, so the reads are complete before the warp converges here): refill it
+            // with the stage NST ahead.
             __syncwarp();
             if (lane == 0) {
+#if NS_FENCE
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#endif
                 issue(slot);
             }
             __syncwarp();
@@ -2073,7 +2165,8 @@ static void launch_nonsep_dmma(mg_plan* Pl, const std::vector<double>& at, cudaS
     const NsAfrag<PP> af = ns_afrag<PP>(at, Pl->p, Pl->P2);
     constexpr int NW = NSD_THREADS / 32;
     const size_t shm = NW * NsStage<PP>::WARP_BYTES + (size_t)NW * Pl->nm * 8 +
-                       (size_t)3 * Pl->nm * 4;
+                       (size_t)(3 * Pl->nm + (Pl->nm & 1)) * 4 +
+                       (NS_ASMEM ? sizeof(NsAfrag<PP>) : 0);
     MG_REQUIRE(shm <= 227 * 1024, "too many modes for the non-separable DMMA kernel");
     static bool attr[64] = {false};
     if (!attr[Pl->device & 63]) {

@@ -483,6 +483,37 @@ def test_large_basis_beyond_32():
     assert frob_rel(got, ref_g) < 1e-12
 
 
+@pytest.mark.parametrize("p", [15, 22, 30])
+def test_every_x_contraction_tile(p, monkeypatch):
+    """Every x-contraction tile (MG_XTILE = 0..7, incl. the N-split forms whose partial last
+    N tile is dealt over the warp columns; a forced N-split tile that does not fit the basis
+    falls back to the automatic choice) against the oracle at the benchmark basis sizes, on a
+    small domain with Nx = 100 (the last k-tile is partial) and a mode subset that keeps the
+    first and last modes."""
+    from dataclasses import replace
+    from paper_1503_08809_b200 import build_qtilde, default_mode_mapping
+    from paper_1503_08809_b200.basis import legendre_on_interval, shifted_legendre
+    lmax = 30
+    hi = host_inputs("c0", l_max=lmax)
+    qk = legendre_on_interval(p, hi.k, hi.spec.k_range[0],
+                              hi.spec.k_range[1] - hi.spec.k_range[0])
+    hi = replace(hi, qk=qk, q=shifted_legendre(p, 2, lmax))
+    C, qt = build_qtilde(hi)
+    full = default_mode_mapping(p).entries
+    rng = np.random.default_rng(p)
+    sub = full[np.unique(np.concatenate([[0, full.shape[0] - 1],
+                                         rng.choice(full.shape[0], 118, replace=False)]))]
+    t = BasisTables(hi.q, qt, C, hi.v, 2, lmax)
+    m = ModeMapping(sub, p)
+    want = ref.gamma3d(hi.q, qt, C, hi.v, hi.wr2, sub, 2, lmax, workers=8, block=32)
+    auto = gamma3d_matrix(t, m, RadialGrid(hi.x)).values
+    assert frob_rel(auto, want) < 1e-12
+    for tile in range(8):
+        monkeypatch.setenv("MG_XTILE", str(tile))
+        got = gamma3d_matrix(t, m, RadialGrid(hi.x)).values
+        assert frob_rel(got, want) < 1e-12, tile
+
+
 def test_distributed_nccl_path_world1(g_c0):
     """The torchrun path (dist.gamma3d_matrix_distributed) with a real NCCL communicator:
     partial Γ written by the plan straight into device memory, all-gathered over NCCL and
