@@ -26,6 +26,12 @@ namespace mg {
 constexpr int QB_XT = MG_QB_XT;       // x values per CTA
 constexpr int QB_KT = 256;            // k per tile (= threads)
 constexpr int QB_LT = 32 / QB_XT;     // l per chunk (XT * LT = 32 output columns)
+#ifndef MG_QB_RECIP
+#define MG_QB_RECIP 1  // sweep recurrences multiply by 1/z (one DMUL + one DFMA per step)
+                       // instead of scipy's operation order with an IEEE division per step
+                       // (mg_bessel.cuh bessel_step, kept for the Bessel table and Δ): the
+                       // division was ~3/4 of the sweep's instructions
+#endif
 #ifndef MG_QB_DMMA
 #define MG_QB_DMMA 1  // contraction over k on DMMA (1) or as per-thread DFMA dot products (0)
 #endif
@@ -34,6 +40,15 @@ constexpr int QB_LT = 32 / QB_XT;     // l per chunk (XT * LT = 32 output column
 constexpr int QB_LDU = MG_QB_DMMA ? QB_KT + 4 : QB_KT + 1;
 constexpr int QB_LDB = MG_QB_DMMA ? QB_KT + 4 : QB_KT;
 constexpr int QB_NC = QB_LT * QB_XT;  // (l, x) output columns per chunk = 32 = 4 n-fragments
+
+// Recurrence step of the q̃ sweeps: j_{l±1} = (2l+1)/z j_l - j_{l∓1}.
+__device__ __forceinline__ double qb_step(int l, double jl, double jother, double z, double rz) {
+#if MG_QB_RECIP
+    return fma((double)(2 * l + 1) * rz, jl, -jother);
+#else
+    return bessel_step(l, jl, jother, z);
+#endif
+}
 
 // Δ[l-l_min][k] for one thread per k (z = X k), plus b[c][k] = wk k^2 qk[c][k].
 __global__ void k_delta(const double* __restrict__ k, const double* __restrict__ wk, int Nk,
@@ -94,7 +109,9 @@ __global__ void k_qb_prepare(const double* __restrict__ k, int Nk, const double*
             st.ua[i] = st.ub[i] = st.da[i] = st.db[i] = 0.0; st.ds[i] = 0;
             continue;
         }
-        BesselNorm bn = bessel_prepare(z, l_max);
+        const double rz = 1.0 / z;
+        auto step = [z, rz](int l, double jl, double jo) { return qb_step(l, jl, jo, z, rz); };
+        BesselNorm bn = bessel_prepare_with(z, l_max, step);
         st.nrm[i] = bn.norm;
         st.lsw[i] = bn.lsw;
         st.stot[i] = bn.stot;
@@ -102,7 +119,7 @@ __global__ void k_qb_prepare(const double* __restrict__ k, int Nk, const double*
         double j0 = MGB_DIV(sin(z), z);
         double jm = j0, jc = MGB_DIV(MGB_SUB(j0, cos(z)), z);  // (j0, j1)
         for (int l = 1; l < l_min - 1; ++l) {
-            double jn = bessel_step(l, jc, jm, z);
+            double jn = step(l, jc, jm);
             jm = jc;
             jc = jn;
         }
@@ -113,7 +130,7 @@ __global__ void k_qb_prepare(const double* __restrict__ k, int Nk, const double*
         int s = 0;
         if (bn.lsw < l_max) {
             for (int l = bn.ls; l > l_max; --l) {
-                double jn = bessel_step(l, jd, jp, z);
+                double jn = step(l, jd, jp);
                 jp = jd;
                 jd = jn;
                 if (fabs(jd) > MGB_BIG) {
@@ -171,7 +188,7 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
             // the XT recurrences of this k advance together (l outer, x inner): XT independent
             // dependency chains per step instead of one long chain per x
             bool okp[QB_XT], live_u[QB_XT];
-            double z[QB_XT];
+            double z[QB_XT], rz[QB_XT];
             int lsw[QB_XT];
             int64_t si[QB_XT];
 #pragma unroll
@@ -180,6 +197,7 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
                 okp[xi] = ki < Nk && xg < Nx;
                 si[xi] = (int64_t)xg * Nk + ki;
                 z[xi] = okp[xi] ? k[ki] * x[xg] : 1.0;
+                rz[xi] = 1.0 / z[xi];
                 lsw[xi] = okp[xi] ? st.lsw[si[xi]] : l_max;
                 live_u[xi] = okp[xi] && z[xi] > 0.0;  // z = 0 contributes nothing
             }
@@ -197,7 +215,7 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
                     for (int xi = 0; xi < QB_XT; ++xi) {
                         double u = 0.0;
                         if (live_u[xi] && li < nl && l <= lsw[xi]) {
-                            const double jn = bessel_step(l - 1, jc[xi], jm[xi], z[xi]);
+                            const double jn = qb_step(l - 1, jc[xi], jm[xi], z[xi], rz[xi]);
                             jm[xi] = jc[xi];
                             jc[xi] = jn;
                             u = dl * jn;
@@ -230,7 +248,7 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
                         if (live_u[xi] && li < nl && l > lsw[xi]) {
                             u = dl * bessel_denorm(jd[xi], sc[xi], bn[xi]);
                             any = true;
-                            const double jn = bessel_step(l, jd[xi], jp[xi], z[xi]);  // jhat_{l-1}
+                            const double jn = qb_step(l, jd[xi], jp[xi], z[xi], rz[xi]);  // jhat_{l-1}
                             jp[xi] = jd[xi];
                             jd[xi] = jn;
                             if (fabs(jd[xi]) > MGB_BIG) {

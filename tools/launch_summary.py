@@ -21,7 +21,7 @@ for r in csv.DictReader(lines):
     tot[name] = tot.get(name, 0.0) + float(r["Metric Value"].replace(",", "")) * scale
     cnt[name] += 1
 live = json.load(open(bench))["roofline"]["kernel_share"]
-fam = {"k_run_contract": "run", "k_x_contract_p": "x", "k_pair_contract": "pair",
+fam = {"k_run_contract": "run", "k_x_contract_p": "x", "k_x_contract_ns": "x", "k_pair_contract": "pair",
        "k_gather": "gather", "k_final": "final"}
 S = sum(tot.values())
 print(f"# ncu launch list: {cmd}")
