@@ -12,6 +12,7 @@
 // recurrence regimes (mg_bessel.cuh): ascending l for l <= l_sw(kx), descending l (Miller,
 // normalised by a pre-pass) for l > l_sw.  Accumulation order is fixed -> deterministic.
 #include <algorithm>
+#include <climits>
 #include <vector>
 
 #include "mg_bessel.cuh"
@@ -31,6 +32,9 @@ constexpr int QB_LT = 32 / QB_XT;     // l per chunk (XT * LT = 32 output column
                        // instead of scipy's operation order with an IEEE division per step
                        // (mg_bessel.cuh bessel_step, kept for the Bessel table and Δ): the
                        // division was ~3/4 of the sweep's instructions
+#endif
+#ifndef MG_QB_SKIP
+#define MG_QB_SKIP 1  // skip (k tile, l chunk) pairs outside the sweep's regime (k_qb_tile_range)
 #endif
 #ifndef MG_QB_DMMA
 #define MG_QB_DMMA 1  // contraction over k on DMMA (1) or as per-thread DFMA dot products (0)
@@ -95,6 +99,8 @@ struct QState {
     double* nrm;
     int* lsw;
     int* stot;
+    int* tmin;  // [x block][k tile]: smallest / largest switch point l_sw in the tile; a sweep
+    int* tmax;  // skips the (k tile, l chunk) pairs that lie wholly outside its regime
 };
 
 __global__ void k_qb_prepare(const double* __restrict__ k, int Nk, const double* __restrict__ x,
@@ -146,6 +152,43 @@ __global__ void k_qb_prepare(const double* __restrict__ k, int Nk, const double*
     }
 }
 
+// Range of the switch points of one (x block, k tile): block (k tile, x block), QB_KT threads.
+// Upward recurrences are live for l <= l_sw, downward ones for l > l_sw, so a chunk starting
+// at l = lc0 has no live recurrence in the tile when lc0 > max l_sw (ascending sweep: every
+// recurrence of the tile has finished) or lc0 <= min l_sw (descending sweep: likewise).  About
+// half of all (k tile, chunk) visits of the two sweeps are such dead pairs.
+__global__ void __launch_bounds__(QB_KT)
+k_qb_tile_range(int Nk, int Nx, QState st) {
+    __shared__ int smin[QB_KT / 32], smax[QB_KT / 32];
+    const int ki = blockIdx.x * QB_KT + threadIdx.x;
+    int lo = INT_MAX, hi = -1;
+    for (int xi = 0; xi < QB_XT; ++xi) {
+        const int xg = blockIdx.y * QB_XT + xi;
+        if (ki < Nk && xg < Nx) {
+            const int v = st.lsw[(int64_t)xg * Nk + ki];
+            lo = min(lo, v);
+            hi = max(hi, v);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        smin[threadIdx.x >> 5] = lo;
+        smax[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < QB_KT / 32; ++w) {
+            lo = min(lo, smin[w]);
+            hi = max(hi, smax[w]);
+        }
+        st.tmin[blockIdx.y * gridDim.x + blockIdx.x] = lo;
+        st.tmax[blockIdx.y * gridDim.x + blockIdx.x] = hi;
+    }
+}
+
 // One sweep (dir = +1 ascending/upward, -1 descending/Miller) over all l for XT x-values.
 // DMMA contraction (MG_QB_DMMA): per chunk, C[c][(l,x)] = Σ_k b[c][k] u[(l,x)][k] with
 // M = p (MF m-fragments), N = 32 (l,x) columns, K = Nk; warp w owns the k-slice
@@ -183,6 +226,12 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #endif
         for (int kt = 0; kt < Nk; kt += QB_KT) {
+#if MG_QB_SKIP
+            {  // CTA-uniform: no recurrence of this k tile is live anywhere in the chunk
+                const int ti = blockIdx.x * ((Nk + QB_KT - 1) / QB_KT) + kt / QB_KT;
+                if (dir > 0 ? st.tmax[ti] < lc0 : lc0 <= st.tmin[ti]) continue;
+            }
+#endif
             const int ki = kt + threadIdx.x;
             bool any = false;
             // the XT recurrences of this k advance together (l outer, x inner): XT independent
@@ -386,14 +435,18 @@ void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x
         const size_t np = (size_t)Nk * Nx;
         DBuf<double> ua(np), ub(np), da(np), dbb(np), nrm(np);
         DBuf<int> ds(np), lsw(np), stot(np);
-        QState st{ua.p, ub.p, da.p, dbb.p, ds.p, nrm.p, lsw.p, stot.p};
         const int grid = (Nx + QB_XT - 1) / QB_XT;
+        const int nkt = (Nk + QB_KT - 1) / QB_KT;
+        DBuf<int> tmin((size_t)grid * nkt), tmax((size_t)grid * nkt);
+        QState st{ua.p, ub.p, da.p, dbb.p, ds.p, nrm.p, lsw.p, stot.p, tmin.p, tmax.p};
         for (int c0 = 0; c0 < p; c0 += QB_PMAX) {  // component blocks: qt is [p][Nx][L]
             const int pb = std::min(QB_PMAX, p - c0);
             const double* bb = db.p + (size_t)c0 * Nk;
             double* qo = qt_dev + (size_t)c0 * Nx * L;
             k_qb_prepare<<<(int)std::min<size_t>((np + 255) / 256, 148 * 64), 256, 0, s>>>(
                 dk.p, Nk, dx.p, Nx, l_min, l_max, st);
+            MG_LAUNCHED();
+            k_qb_tile_range<<<dim3(nkt, grid), QB_KT, 0, s>>>(Nk, Nx, st);
             MG_LAUNCHED();
             const int mf = (pb + 7) / 8;
             const size_t shm = (size_t)(QB_LT * QB_XT * QB_LDU + (MG_QB_DMMA ? mf * 8 : pb) * QB_LDB) *
