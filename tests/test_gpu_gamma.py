@@ -514,6 +514,30 @@ def test_every_x_contraction_tile(p, monkeypatch):
         assert frob_rel(got, want) < 1e-12, tile
 
 
+@pytest.mark.parametrize("p", [7, 10, 13, 16, 18, 19, 21, 24, 27, 32])
+def test_basis_sizes_automatic_tile(p):
+    """Basis sizes between the benchmark ones: whatever x-contraction tile choose_xtile picks
+    (plain or N-split, partial M and N tiles, 1 to 3 n-fragments dealt per warp column) against
+    the oracle on a small domain with a 60-mode subset mapping."""
+    from dataclasses import replace
+    from paper_1503_08809_b200 import build_qtilde, default_mode_mapping
+    from paper_1503_08809_b200.basis import legendre_on_interval, shifted_legendre
+    lmax = 22
+    hi = host_inputs("c0", l_max=lmax)
+    qk = legendre_on_interval(p, hi.k, hi.spec.k_range[0],
+                              hi.spec.k_range[1] - hi.spec.k_range[0])
+    hi = replace(hi, qk=qk, q=shifted_legendre(p, 2, lmax))
+    C, qt = build_qtilde(hi)
+    full = default_mode_mapping(p).entries
+    rng = np.random.default_rng(100 + p)
+    sub = full[np.unique(np.concatenate([[0, full.shape[0] - 1],
+                                         rng.choice(full.shape[0], 58, replace=False)]))]
+    got = gamma3d_matrix(BasisTables(hi.q, qt, C, hi.v, 2, lmax), ModeMapping(sub, p),
+                         RadialGrid(hi.x)).values
+    want = ref.gamma3d(hi.q, qt, C, hi.v, hi.wr2, sub, 2, lmax, workers=4, block=32)
+    assert frob_rel(got, want) < 1e-12
+
+
 def test_distributed_nccl_path_world1(g_c0):
     """The torchrun path (dist.gamma3d_matrix_distributed) with a real NCCL communicator:
     partial Γ written by the plan straight into device memory, all-gathered over NCCL and
