@@ -159,24 +159,30 @@ def native_maps() -> list:
 
 # ------------------------------------------------------------------------------------------
 def cpu_rate(hi, qt_host, C, seconds, cores):
-    """Oracle port (= reference _sweep_chunk code path) on a bounded flat slice, all cores."""
+    """Oracle port (= reference _sweep_chunk code path) on bounded flat slices at 10 %, 50 % and
+    90 % of the triple index (per-triple work n·Nx is uniform, so the rate
+    extrapolates linearly in T), all cores, per-call pool setup measured on an empty range and
+    subtracted."""
     from oracle import ref
 
     T = ref.domain_count(2, hi.l_max)
     n = hi.entries.shape[0]
     per_core = 1.5e7                                  # upd/s/core, SURVEY §6 (c0..c4 slices)
-    S = max(cores * 8, int(seconds * per_core * cores / (hi.x.size * n)))
-    S = min(S, T)
-    a = T // 2
-    t0 = time.perf_counter()
-    ref.gamma3d(hi.q, qt_host, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max, a, a + S,
-                workers=cores, block=64)
-    dt = time.perf_counter() - t0
+    S = max(cores * 8, int(seconds / 3 * per_core * cores / (hi.x.size * n)))
+    S = min(S, T // 3)
+    starts = [min(int(f * T), T - S) for f in (0.1, 0.5, 0.9)]
+    dt = 0.0
+    for a in starts:
+        t0 = time.perf_counter()
+        ref.gamma3d(hi.q, qt_host, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max, a, a + S,
+                    workers=cores, block=64)
+        dt += time.perf_counter() - t0
+    a = starts[1]
     t0 = time.perf_counter()                    # per-call pool setup (empty range), subtracted
     ref.gamma3d(hi.q, qt_host, C, hi.v, hi.wr2, hi.entries, 2, hi.l_max, a, a,
                 workers=cores, block=64)
-    dt = max(dt - (time.perf_counter() - t0), 1e-9)
-    return S * hi.x.size * n / dt, S, a, dt
+    dt = max(dt - 3 * (time.perf_counter() - t0), 1e-9)
+    return 3 * S * hi.x.size * n / dt, S, starts, dt
 
 
 def run_nonsep(args):
@@ -504,8 +510,9 @@ def run_b200(args):
             "value": rate, "unit": "updates/s", "cores": cores, "kind": "port",
             "cpu_model": cpu_model(),
             "sample": f"oracle port of engine3d._sweep_chunk (B=64, fork pool of {cores}) over "
-                      f"flat range [{a0}, {a0 + S}) of config {args.config[1:]} "
-                      f"({S} triples, {dt:.1f} s); extrapolated s/Γ = {U / rate:.3g}"}
+                      f"3 flat ranges of {S} triples starting at {a0} (10/50/90 % of the index) "
+                      f"of config {args.config[1:]} ({3 * S} triples, {dt:.1f} s); "
+                      f"extrapolated s/Γ = {U / rate:.3g}"}
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()

@@ -33,6 +33,9 @@ constexpr int QB_LT = 32 / QB_XT;     // l per chunk (XT * LT = 32 output column
                        // (mg_bessel.cuh bessel_step, kept for the Bessel table and Δ): the
                        // division was ~3/4 of the sweep's instructions
 #endif
+#ifndef MG_QB_PREFETCH
+#define MG_QB_PREFETCH 1  // load a chunk's Δ_l(k) values before its recurrence steps
+#endif
 #ifndef MG_QB_SKIP
 #define MG_QB_SKIP 1  // skip (k tile, l chunk) pairs outside the sweep's regime (k_qb_tile_range)
 #endif
@@ -195,7 +198,7 @@ k_qb_tile_range(int Nk, int Nx, QState st) {
 // [32w, 32w+32) of every k-tile and all MF x 4 output fragments; the 8 warp partials are
 // summed in warp order at the end of the chunk (deterministic).
 template <int MF>
-__global__ void __launch_bounds__(QB_KT)
+__global__ void __launch_bounds__(QB_KT, MF <= 2 ? 2 : 1)  // 2 CTAs per SM while the tiles fit
 k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restrict__ x, int Nx,
            const double* __restrict__ delta, const double* __restrict__ b, int p, int l_min,
            int l_max, QState st, double* __restrict__ qt) {
@@ -250,6 +253,22 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
                 lsw[xi] = okp[xi] ? st.lsw[si[xi]] : l_max;
                 live_u[xi] = okp[xi] && z[xi] > 0.0;  // z = 0 contributes nothing
             }
+            // the chunk's Δ_l(k) values up front: QB_LT independent loads in flight at once
+            // (inside the recurrence loop they were issued a few at a time and each group
+            // paid an L2 round trip with only 2-4 warps per sub-partition to hide it)
+#if MG_QB_PREFETCH
+            double dlv[QB_LT];
+#pragma unroll
+            for (int li = 0; li < QB_LT; ++li)
+                dlv[li] = li < nl ? __ldg(delta + (int64_t)(lc0 + dir * li - l_min) * Nk +
+                                          min(ki, Nk - 1))
+                                  : 0.0;
+#define QB_DL(li, l) dlv[li]
+#define QB_UNROLL _Pragma("unroll")
+#else
+#define QB_DL(li, l) ((li) < nl ? delta[(int64_t)((l) - l_min) * Nk + min(ki, Nk - 1)] : 0.0)
+#define QB_UNROLL
+#endif
             if (dir > 0) {
                 double jm[QB_XT], jc[QB_XT];
 #pragma unroll
@@ -257,9 +276,10 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
                     jm[xi] = okp[xi] ? st.ua[si[xi]] : 0.0;
                     jc[xi] = okp[xi] ? st.ub[si[xi]] : 0.0;
                 }
+QB_UNROLL
                 for (int li = 0; li < QB_LT; ++li) {
                     const int l = lc0 + li;
-                    const double dl = li < nl ? delta[(int64_t)(l - l_min) * Nk + min(ki, Nk - 1)] : 0.0;
+                    const double dl = QB_DL(li, l);
 #pragma unroll
                     for (int xi = 0; xi < QB_XT; ++xi) {
                         double u = 0.0;
@@ -288,9 +308,10 @@ k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restri
                     bn[xi].norm = okp[xi] ? st.nrm[si[xi]] : 0.0;
                     bn[xi].stot = okp[xi] ? st.stot[si[xi]] : 0;
                 }
+QB_UNROLL
                 for (int li = 0; li < QB_LT; ++li) {
                     const int l = lc0 - li;
-                    const double dl = li < nl ? delta[(int64_t)(l - l_min) * Nk + min(ki, Nk - 1)] : 0.0;
+                    const double dl = QB_DL(li, l);
 #pragma unroll
                     for (int xi = 0; xi < QB_XT; ++xi) {
                         double u = 0.0;
