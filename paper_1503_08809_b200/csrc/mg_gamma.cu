@@ -634,6 +634,9 @@ template <class Cfg>
 static void launch_x_ns(int num_sms, cudaStream_t st, const double* S, const double* H, int nrows,
                         int row_b1, int row_b3, int p, int P2, int Nx, int NxP, double* G,
                         const MgBounds& bd) {
+    MG_REQUIRE(nsplit_efficiency<Cfg>(P2, p * p) > 0.0,
+               "N-split x tile does not fit this basis size (a warp column would get fewer "
+               "than FN - 2 n-fragments)");
     k_x_contract_ns<Cfg><<<num_sms, XPipeNS<Cfg>::THREADS, XPipeNS<Cfg>::smem_bytes, st>>>(
         S, H, nrows, row_b1, row_b3, p, P2, Nx, NxP, G, bd);
 }
