@@ -25,7 +25,10 @@ namespace mg {
 #define MG_QB_XT 2  // measured: 2 beats 4 at c1 (0.042 vs 0.056 s), ties at c4; 1 is slower
 #endif
 constexpr int QB_XT = MG_QB_XT;       // x values per CTA
-constexpr int QB_KT = 256;            // k per tile (= threads)
+#ifndef MG_QB_KT
+#define MG_QB_KT 256
+#endif
+constexpr int QB_KT = MG_QB_KT;       // k per tile (= threads)
 constexpr int QB_LT = 32 / QB_XT;     // l per chunk (XT * LT = 32 output columns)
 #ifndef MG_QB_RECIP
 #define MG_QB_RECIP 1  // sweep recurrences multiply by 1/z (one DMUL + one DFMA per step)
@@ -35,6 +38,11 @@ constexpr int QB_LT = 32 / QB_XT;     // l per chunk (XT * LT = 32 output column
 #endif
 #ifndef MG_QB_PREFETCH
 #define MG_QB_PREFETCH 1  // load a chunk's Δ_l(k) values before its recurrence steps
+#endif
+// resident CTAs per SM the register allocation must allow: the shared-memory tiles of MF
+// m-fragments ((32 + 8 MF) rows of QB_KT + 4 doubles) decide how many actually fit
+#ifndef MG_QB_MINB
+#define MG_QB_MINB(MF) ((MF) <= 2 ? 2 : 1)
 #endif
 #ifndef MG_QB_SKIP
 #define MG_QB_SKIP 1  // skip (k tile, l chunk) pairs outside the sweep's regime (k_qb_tile_range)
@@ -198,7 +206,7 @@ k_qb_tile_range(int Nk, int Nx, QState st) {
 // [32w, 32w+32) of every k-tile and all MF x 4 output fragments; the 8 warp partials are
 // summed in warp order at the end of the chunk (deterministic).
 template <int MF>
-__global__ void __launch_bounds__(QB_KT, MF <= 2 ? 2 : 1)  // 2 CTAs per SM while the tiles fit
+__global__ void __launch_bounds__(QB_KT, MG_QB_MINB(MF))
 k_qb_sweep(int dir, const double* __restrict__ k, int Nk, const double* __restrict__ x, int Nx,
            const double* __restrict__ delta, const double* __restrict__ b, int p, int l_min,
            int l_max, QState st, double* __restrict__ qt) {
@@ -430,7 +438,7 @@ void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x
     MG_REQUIRE(Nk >= 1 && Nx >= 1 && p >= 1, "Nk, Nx, p must be >= 1");
     // the sweep kernel holds up to QB_PMAX components (4 DMMA m-fragments); larger bases are
     // built in component blocks (each block re-runs the Bessel recurrences)
-    constexpr int QB_PMAX = 4 * QB_KT / (QB_XT * QB_LT);
+    constexpr int QB_PMAX = MG_QB_DMMA ? 32 : 4 * QB_KT / (QB_XT * QB_LT);
     for (int i = 0; i < Nk; ++i) MG_REQUIRE(k[i] > 0, "k grid must be > 0");
     const int L = l_max - l_min + 1;
     DBuf<double> dk, dwk, dx, deps, dqk, ddelta, db;
