@@ -213,6 +213,28 @@ class TestHarness:
                                                              r_samples=60))
         assert rep.max_rel_dev <= 1e-10
 
+    def test_run_convergence_study(self, monkeypatch):
+        """harness.run_convergence_study (harness.py:312-340): every integrator on a ladder of
+        radial grids against the dense-spline gold standard, all through the rebound engine;
+        the percentage RMSEs must equal the reference's own."""
+        cfg = cp.harness.RunConfig(l_max=14, p_max=3, r_samples=54)
+        got = cp.harness.run_convergence_study(cfg, ladder=(54, 108))
+        monkeypatch.undo()
+        want = cp.harness.run_convergence_study(cfg, ladder=(54, 108))
+        assert [(r["integrator"], r["r_samples"]) for r in got] == \
+               [(r["integrator"], r["r_samples"]) for r in want]
+        for a, b in zip(got, want):
+            assert abs(a["rmse_percent"] - b["rmse_percent"]) <= 1e-8 * max(1.0, b["rmse_percent"])
+
+    def test_run_bench(self):
+        """harness.run_bench (harness.py:353-410) drives the 2D engine and the direct engine
+        with an explicit enumerate_domain() object and a worker count through the rebinding."""
+        rows = cp.harness.run_bench(cp.harness.RunConfig(l_max=16, p_max=3, r_samples=54,
+                                                         workers=2, bench_repeats=1))
+        assert [r["path"] for r in rows] == ["2d-optimized", "2d-naive", "2d-speedup", "3d-w1",
+                                             "3d-w2"]
+        assert all(r["seconds"] == "" or r["seconds"] > 0 for r in rows)
+
     def test_serialize_roundtrip(self, tmp_path, desk):
         g = cp.gamma3d_matrix(desk.tables, desk.mapping, desk.grid)
         for fmt in ("csv", "bin"):
