@@ -235,6 +235,20 @@ class TestHarness:
                                              "3d-w2"]
         assert all(r["seconds"] == "" or r["seconds"] > 0 for r in rows)
 
+    def test_cli_end_to_end(self, tmp_path, monkeypatch, capsys):
+        """The reference's command line (cli.py:105-148) reaches the GPU through the same
+        rebinding: `--mode gamma3d --out ...` writes the matrix the reference itself writes."""
+        import cmbproj.cli as cli
+        args = ["--mode", "gamma3d", "--lmax", "18", "--pmax", "3", "--r-samples", "54",
+                "--format", "bin"]
+        assert cli.main(args + ["--out", str(tmp_path / "gpu.bin")]) == 0
+        monkeypatch.undo()
+        assert cli.main(args + ["--out", str(tmp_path / "cpu.bin")]) == 0
+        a = cp.harness.deserialize_gamma(tmp_path / "gpu.bin", "bin")
+        b = cp.harness.deserialize_gamma(tmp_path / "cpu.bin", "bin")
+        assert relative_gap(a.values, b.values) < 1e-12
+        assert "wrote 10x10 matrix" in capsys.readouterr().out
+
     def test_serialize_roundtrip(self, tmp_path, desk):
         g = cp.gamma3d_matrix(desk.tables, desk.mapping, desk.grid)
         for fmt in ("csv", "bin"):
