@@ -7,8 +7,7 @@
 //     (gamma2d_entry, :112-129: μ first, then the radial rule)
 // The P table is built with the reference's exact operation order (term = ((lw q_a) q̃_b) P_l,
 // Kahan update y = term - comp; t = acc + y; comp = (t - acc) - y), each FP64 op an explicit
-// round-to-nearest intrinsic, so it reproduces the reference table bit for bit.  The cell
-// kernel stages P[:, :, x, μ-chunk] in shared memory and gives every thread one Γ cell.
+// round-to-nearest intrinsic, so it reproduces the reference table bit for bit.
 #include <algorithm>
 #include <vector>
 
@@ -16,74 +15,147 @@
 
 namespace mg {
 
-// P[((a*p + b)*Nx + x)*nmu + m], one thread per element, sequential Kahan over l.
-__global__ void k_ptable(const double* __restrict__ q, const double* __restrict__ qt,
-                         const double* __restrict__ lw, const double* __restrict__ leg, int p,
-                         int Nx, int L, int nmu, double* __restrict__ P) {
-    const int64_t total = (int64_t)p * p * Nx * nmu;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int m = (int)(i % nmu);
-        int64_t r = i / nmu;
-        const int x = (int)(r % Nx);
-        r /= Nx;
-        const int b = (int)(r % p), a = (int)(r / p);
-        const double* qa = q + (int64_t)a * L;
-        const double* qb = qt + ((int64_t)b * Nx + x) * L;
-        double acc = 0.0, comp = 0.0;
-        for (int l = 0; l < L; ++l) {
-            const double lwq = __dmul_rn(lw[l], qa[l]);
-            const double term = __dmul_rn(__dmul_rn(lwq, qb[l]), leg[(int64_t)l * nmu + m]);
-            const double y = __dsub_rn(term, comp);
-            const double t = __dadd_rn(acc, y);
-            comp = __dsub_rn(__dsub_rn(t, acc), y);
-            acc = t;
+// ---- P table -----------------------------------------------------------------------------
+// P[((a*p + b)*Nx + x)*nmu + m] as a register-tiled product over l: rows r = (a, b, x), columns
+// m, a CTA owns a 64 x 64 tile and walks l in ascending chunks of PT_BK staged through shared
+// memory (A[r][l] = (lw_l q_a(l)) q̃_b(x,l) formed once per element with the reference's two
+// roundings, B[l][m] = P_l(μ_m)); a thread keeps a 4 x 4 block of (sum, compensation) pairs,
+// so one staged A/B value feeds four Kahan updates.  Each output still sees exactly the
+// reference's sequence of rounded operations in ascending l: the table is bit-identical.
+constexpr int PT_BM = 64, PT_BN = 64, PT_BK = 32;
+
+__global__ void __launch_bounds__(256)
+k_ptable_tiled(const double* __restrict__ q, const double* __restrict__ qt,
+               const double* __restrict__ lw, const double* __restrict__ leg, int p, int Nx,
+               int L, int nmu, double* __restrict__ P) {
+    __shared__ double As[PT_BK][PT_BM + 1];  // odd stride: the transposing store is conflict-free
+    __shared__ double Bs[PT_BK][PT_BN];
+    const int64_t R = (int64_t)p * p * Nx;
+    const int64_t r0 = (int64_t)blockIdx.y * PT_BM;
+    const int m0 = blockIdx.x * PT_BN;
+    const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+    double acc[4][4], comp[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = comp[i][j] = 0.0;
+
+    // this thread's staging slots: A rows (t/32 + 8 i) at l-offset t%32; B row t/64 + 4 i at
+    // column t%64
+    const int al = t & 31, ar = t >> 5;
+    const double* arow[8];
+    const double* aq[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t r = r0 + ar + 8 * i;
+        if (r < R) {
+            const int x = (int)(r % Nx);
+            const int ab = (int)(r / Nx);
+            arow[i] = qt + ((int64_t)(ab % p) * Nx + x) * L;
+            aq[i] = q + (int64_t)(ab / p) * L;
+        } else {
+            arow[i] = nullptr;
+            aq[i] = nullptr;
         }
-        P[i] = acc;
+    }
+    const int bc = t & 63, bl = t >> 6;
+    const bool bok = m0 + bc < nmu;
+
+    for (int l0 = 0; l0 < L; l0 += PT_BK) {
+        const int kn = min(PT_BK, L - l0);
+        __syncthreads();
+        {
+            const int l = l0 + al;
+            const double w = l < L ? lw[l] : 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double v = 0.0;
+                if (l < L && arow[i]) v = __dmul_rn(__dmul_rn(w, aq[i][l]), arow[i][l]);
+                As[al][ar + 8 * i] = v;
+            }
+#pragma unroll
+            for (int i = 0; i < PT_BK / 4; ++i) {
+                const int l2 = l0 + bl + 4 * i;
+                Bs[bl + 4 * i][bc] = (bok && l2 < L) ? leg[(int64_t)l2 * nmu + m0 + bc] : 0.0;
+            }
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kn; ++kk) {  // never past L: a padded step would still apply comp
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double term = __dmul_rn(a[i], b[j]);
+                    const double y = __dsub_rn(term, comp[i][j]);
+                    const double s = __dadd_rn(acc[i][j], y);
+                    comp[i][j] = __dsub_rn(__dsub_rn(s, acc[i][j]), y);
+                    acc[i][j] = s;
+                }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t r = r0 + ty * 4 + i;
+        if (r >= R) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int m = m0 + tx + 16 * j;
+            if (m < nmu) P[r * nmu + m] = acc[i][j];
+        }
     }
 }
 
+// ---- Γ cells --------------------------------------------------------------------------------
+// A CTA owns a 16 x 16 tile of (n, n') cells and one contiguous chunk of the radial points
+// (grid.z): for each x it stages P[:, :, x, μ-chunk] transposed ([μ][a*p+b], odd row stride) so
+// the nine operands of a cell's 3 x 3 matrix are read at (r_i, c_j) offsets of one short row,
+// sums the permanent against the μ rule, then adds w_x r_x² times that to the chunk's partial.
+// k_gamma2d_reduce adds the chunk partials in ascending x order (deterministic for a given
+// split) and applies 1/(48π).
 constexpr int G2_TILE = 16;  // 16 x 16 cells per CTA
 
 __global__ void __launch_bounds__(G2_TILE* G2_TILE)
 k_gamma2d_cells(const double* __restrict__ P, const int* __restrict__ modes, int n, int p,
-                int Nx, int nmu, int mc, const double* __restrict__ mu_w,
-                const double* __restrict__ wr2, double* __restrict__ gamma) {
-    extern __shared__ double sp[];  // [p*p][mc]
+                int Nx, int nmu, int mc, int ps, int xsplit, const double* __restrict__ mu_w,
+                const double* __restrict__ wr2, double* __restrict__ partial) {
+    extern __shared__ double sp[];  // [mc][ps]
     const int tn = threadIdx.x / G2_TILE, tq = threadIdx.x % G2_TILE;
     const int nrow = blockIdx.y * G2_TILE + tn, ncol = blockIdx.x * G2_TILE + tq;
     const bool ok = nrow < n && ncol < n;
-    int r0 = 0, r1 = 0, r2 = 0, c0 = 0, c1 = 0, c2 = 0;
+    int o[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (ok) {
-        r0 = modes[3 * nrow]; r1 = modes[3 * nrow + 1]; r2 = modes[3 * nrow + 2];
-        c0 = modes[3 * ncol]; c1 = modes[3 * ncol + 1]; c2 = modes[3 * ncol + 2];
+        const int r[3] = {modes[3 * nrow], modes[3 * nrow + 1], modes[3 * nrow + 2]};
+        const int c[3] = {modes[3 * ncol], modes[3 * ncol + 1], modes[3 * ncol + 2]};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) o[3 * i + j] = r[i] * p + c[j];
     }
     const int pp = p * p;
+    const int xa = (int)((int64_t)Nx * blockIdx.z / xsplit);
+    const int xb = (int)((int64_t)Nx * (blockIdx.z + 1) / xsplit);
     double acc = 0.0;
-    for (int x = 0; x < Nx; ++x) {
+    for (int x = xa; x < xb; ++x) {
         double inner = 0.0;
         for (int m0 = 0; m0 < nmu; m0 += mc) {
             const int mn = min(mc, nmu - m0);
             __syncthreads();
-            for (int e = threadIdx.x; e < pp * mc; e += blockDim.x) {
-                const int ab = e / mc, mm = e % mc;
-                sp[e] = mm < mn ? P[((int64_t)ab * Nx + x) * nmu + m0 + mm] : 0.0;
+            for (int e = threadIdx.x; e < pp * mn; e += blockDim.x) {
+                const int ab = e / mn, mm = e - ab * mn;
+                sp[mm * ps + ab] = P[((int64_t)ab * Nx + x) * nmu + m0 + mm];
             }
             __syncthreads();
             if (ok) {
-                const double* s00 = sp + (r0 * p + c0) * mc;
-                const double* s01 = sp + (r0 * p + c1) * mc;
-                const double* s02 = sp + (r0 * p + c2) * mc;
-                const double* s10 = sp + (r1 * p + c0) * mc;
-                const double* s11 = sp + (r1 * p + c1) * mc;
-                const double* s12 = sp + (r1 * p + c2) * mc;
-                const double* s20 = sp + (r2 * p + c0) * mc;
-                const double* s21 = sp + (r2 * p + c1) * mc;
-                const double* s22 = sp + (r2 * p + c2) * mc;
-                for (int mm = 0; mm < mn; ++mm) {
-                    const double m00 = s00[mm], m01 = s01[mm], m02 = s02[mm];
-                    const double m10 = s10[mm], m11 = s11[mm], m12 = s12[mm];
-                    const double m20 = s20[mm], m21 = s21[mm], m22 = s22[mm];
+                const double* s = sp;
+                for (int mm = 0; mm < mn; ++mm, s += ps) {
+                    const double m00 = s[o[0]], m01 = s[o[1]], m02 = s[o[2]];
+                    const double m10 = s[o[3]], m11 = s[o[4]], m12 = s[o[5]];
+                    const double m20 = s[o[6]], m21 = s[o[7]], m22 = s[o[8]];
                     // engine2d.py:101-109 term order
                     const double per = m00 * m11 * m22 + m00 * m12 * m21 + m01 * m10 * m22 +
                                        m01 * m12 * m20 + m02 * m10 * m21 + m02 * m11 * m20;
@@ -93,7 +165,16 @@ k_gamma2d_cells(const double* __restrict__ P, const int* __restrict__ modes, int
         }
         acc += wr2[x] * inner;
     }
-    if (ok) gamma[(int64_t)nrow * n + ncol] = acc / (48.0 * 3.141592653589793);
+    if (ok) partial[((int64_t)blockIdx.z * n + nrow) * n + ncol] = acc;
+}
+
+__global__ void k_gamma2d_reduce(const double* __restrict__ partial, int64_t cells, int xsplit,
+                                 double* __restrict__ gamma) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= cells) return;
+    double acc = 0.0;
+    for (int z = 0; z < xsplit; ++z) acc += partial[z * cells + i];
+    gamma[i] = acc / (48.0 * 3.141592653589793);
 }
 
 void ptable_dev(const double* q, const double* qt, const double* lw, const double* leg, int p,
@@ -103,29 +184,47 @@ void ptable_dev(const double* q, const double* qt, const double* lw, const doubl
     dqt.upload(qt, (size_t)p * Nx * L);
     dlw.upload(lw, L);
     dleg.upload(leg, (size_t)L * nmu);
-    const int64_t total = (int64_t)p * p * Nx * nmu;
-    k_ptable<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 64), 256>>>(
-        dq.p, dqt.p, dlw.p, dleg.p, p, Nx, L, nmu, P_dev);
+    const int64_t R = (int64_t)p * p * Nx;
+    MG_REQUIRE(ceil_div(R, PT_BM) <= 65535, "P table has too many (a, b, x) rows");
+    dim3 grid(ceil_div(nmu, PT_BN), ceil_div(R, PT_BM));
+    k_ptable_tiled<<<grid, 256>>>(dq.p, dqt.p, dlw.p, dleg.p, p, Nx, L, nmu, P_dev);
     MG_LAUNCHED();
     MG_CUDA(cudaDeviceSynchronize());
+}
+
+// x chunks per cell tile: enough CTAs for ~4 per SM, at most one chunk per radial point and
+// at most 1 GiB of partials.
+int gamma2d_xsplit(int n, int Nx) {
+    const int64_t tiles = (int64_t)ceil_div(n, G2_TILE) * ceil_div(n, G2_TILE);
+    int64_t xs = (148 * 4 + tiles - 1) / tiles;
+    xs = std::min<int64_t>(xs, Nx);
+    xs = std::min<int64_t>(xs, std::max<int64_t>(1, (int64_t(1) << 27) / ((int64_t)n * n)));
+    return (int)std::max<int64_t>(1, xs);
 }
 
 void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int Nx, int nmu,
                  const double* mu_w, const double* wr2, double* gamma_host) {
     DBuf<int> dm;
-    DBuf<double> dw, dr, dg;
+    DBuf<double> dw, dr, dg, dpart;
     dm.upload(modes_host, 3 * (size_t)n);
     dw.upload(mu_w, nmu);
     dr.upload(wr2, Nx);
     dg.alloc((size_t)n * n);
-    const int mc = std::max(1, std::min(32, 12288 / (p * p)));
-    const size_t shm = (size_t)p * p * mc * sizeof(double);
+    const int xsplit = gamma2d_xsplit(n, Nx);
+    dpart.alloc((size_t)xsplit * n * n);
+    const int ps = (p * p) | 1;
+    const int mc = std::max(1, std::min(std::min(64, nmu), 12288 / ps));
+    const size_t shm = (size_t)ps * mc * sizeof(double);
     if (shm > 48 * 1024)
         MG_CUDA(cudaFuncSetAttribute(k_gamma2d_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)shm));
-    dim3 grid(ceil_div(n, G2_TILE), ceil_div(n, G2_TILE));
-    k_gamma2d_cells<<<grid, G2_TILE * G2_TILE, shm>>>(P_dev, dm.p, n, p, Nx, nmu, mc, dw.p,
-                                                        dr.p, dg.p);
+    MG_REQUIRE(ceil_div(n, G2_TILE) <= 65535, "too many modes for the cell grid");
+    dim3 grid(ceil_div(n, G2_TILE), ceil_div(n, G2_TILE), xsplit);
+    k_gamma2d_cells<<<grid, G2_TILE * G2_TILE, shm>>>(P_dev, dm.p, n, p, Nx, nmu, mc, ps, xsplit,
+                                                        dw.p, dr.p, dpart.p);
+    MG_LAUNCHED();
+    const int64_t cells = (int64_t)n * n;
+    k_gamma2d_reduce<<<ceil_div(cells, 256), 256>>>(dpart.p, cells, xsplit, dg.p);
     MG_LAUNCHED();
     MG_CUDA(cudaMemcpy(gamma_host, dg.p, (size_t)n * n * sizeof(double),
                        cudaMemcpyDeviceToHost));

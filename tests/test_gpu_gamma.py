@@ -331,6 +331,28 @@ class TestGamma2D:
         g3 = gamma3d_matrix(t, m, r, h2_mode="exact").values
         assert gap_rel(got.values, g3) < 1e-10
 
+    @pytest.mark.parametrize("lmin,lmax,p,nx,nmu", [(2, 70, 5, 37, 107),    # 3 l chunks, 2 μ tiles
+                                                     (3, 34, 7, 19, 65),     # 33 = 32 + 1 rows of l
+                                                     (2, 150, 3, 130, 228)])  # 19 row tiles
+    def test_tiled_kernels_vs_oracle(self, lmin, lmax, p, nx, nmu):
+        """Sizes that cross every tile edge of the P-table kernel (64 x 64 x 32: partial row,
+        column and l tiles) and of the cell kernel (x chunks per CTA, μ chunks of 64, partial
+        16 x 16 cell tiles) against oracle/gamma2d_ref.py (pinned to the reference's tables)."""
+        from oracle import gamma2d_ref
+        from paper_1503_08809_b200 import (build_ptable, default_mode_mapping, gamma2d_matrix,
+                                           gauss_legendre, legendre_table)
+        t, r = TestEdgeCases().random_tables(lmin, lmax, p, nx, seed=11)
+        m = default_mode_mapping(p)
+        rule = gauss_legendre(nmu)
+        leg = legendre_table(lmax, rule)
+        want_p = gamma2d_ref.ptable(t.q, t.q_tilde, t.C, t.v, lmin, lmax, leg)
+        pt = build_ptable(t, r, rule, leg)
+        assert np.array_equal(pt.values, want_p)
+        want = gamma2d_ref.gamma2d(want_p, m.entries, rule.weights, x_weights(r.r))
+        got = gamma2d_matrix(t, m, r, rule, leg).values
+        assert gap_rel(got, want) < 1e-12
+        assert np.array_equal(gamma2d_matrix(t, m, r, rule, leg, ptable=pt).values, got)
+
     def test_budget_and_errors(self, g_desk):
         from paper_1503_08809_b200 import build_ptable, gauss_legendre, legendre_table
         t, m, r = desk_problem(g_desk, "desk")

@@ -176,3 +176,25 @@ class TestNonsepPin:
         l3 = np.array([2, 3, 4, 25])          # even ok, odd sum, odd sum, no triangle
         h = ref.h2_exact(l1, l2, l3)
         assert h[0] > 0 and h[1] == 0 and h[2] == 0 and h[3] == 0
+
+
+class TestGamma2DPin:
+    """oracle/gamma2d_ref.py against the reference's own P tables and Γ2d matrices
+    (tests/golden/io2d.npz, written by cmbproj.build_ptable / gamma2d_matrix)."""
+
+    @pytest.mark.parametrize("tag", ["desk", "desk32"])
+    def test_ptable_and_gamma2d(self, g_desk, tag):
+        from conftest import golden
+        from oracle import gamma2d_ref
+        from paper_1503_08809_b200.quadrature import gauss_legendre, legendre_table
+        g2 = golden("io2d.npz")
+        lmin, lmax = (int(x) for x in g_desk[f"{tag}_lrange"])
+        rule = gauss_legendre(g2[f"{tag}_mu_nodes"].size)
+        assert np.array_equal(rule.weights, g2[f"{tag}_mu_weights"])
+        leg = legendre_table(lmax, rule)
+        P = gamma2d_ref.ptable(g_desk[f"{tag}_q"], g_desk[f"{tag}_qt"], g_desk[f"{tag}_C"],
+                               g_desk[f"{tag}_v"], lmin, lmax, leg)
+        assert np.array_equal(P, g2[f"{tag}_ptable"])
+        wr2 = x_weights(g_desk[f"{tag}_r"], "trap")
+        got = gamma2d_ref.gamma2d(P, g_desk[f"{tag}_entries"], rule.weights, wr2)
+        assert gap_rel(got, g2[f"{tag}_gamma2d"]) < 1e-13

@@ -30,6 +30,7 @@ ap.add_argument("--lmax", type=int, default=128)
 ap.add_argument("--pmax", type=int, default=4)
 ap.add_argument("--r", type=int, default=216)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--no-ref", action="store_true", help="skip the CPU reference (large sizes)")
 a = ap.parse_args()
 grid = cp.default_radial_grid(a.r)
 tables = cp.synthesize_basis(a.pmax, 2, a.lmax, grid)
@@ -47,6 +48,18 @@ for i in range(a.reps + 1):
 t0 = time.perf_counter()
 pt = build_ptable(tables, grid, rule, leg)
 t_pt = time.perf_counter() - t0
+if a.no_ref:
+    # executed FP64 operations: P table 5 per (element, l) (1 mul + 4 Kahan adds; the A operand's
+    # two multiplies are shared by a row), cells 23 per (cell, x, μ) (12 mul + 5 add of the
+    # permanent, 1 FMA of the μ rule, counted as issued instructions)
+    print(json.dumps({
+        "engine": "modal2d (mu quadrature)", "l_max": a.lmax, "p_max": a.pmax, "n_r": a.r,
+        "n_mu": rule.n, "n_modes": mapping.n_max, "gpu_s": float(np.median(gpu)),
+        "gpu_ptable_s": t_pt,
+        "ptable_ops": 5.0 * a.pmax ** 2 * a.r * rule.n * (a.lmax - 1),
+        "cell_ops": 23.0 * mapping.n_max ** 2 * a.r * rule.n,
+        "ptable_bytes": 8.0 * a.pmax ** 2 * a.r * rule.n}))
+    sys.exit(0)
 ref = []
 for i in range(max(1, a.reps // 2)):
     t0 = time.perf_counter()
