@@ -9,6 +9,7 @@
 // Kahan update y = term - comp; t = acc + y; comp = (t - acc) - y), each FP64 op an explicit
 // round-to-nearest intrinsic, so it reproduces the reference table bit for bit.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "mg_common.cuh"
@@ -24,7 +25,7 @@ namespace mg {
 // reference's sequence of rounded operations in ascending l: the table is bit-identical.
 constexpr int PT_BM = 64, PT_BN = 64, PT_BK = 32;
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 k_ptable_tiled(const double* __restrict__ q, const double* __restrict__ qt,
                const double* __restrict__ lw, const double* __restrict__ leg, int p, int Nx,
                int L, int nmu, double* __restrict__ P) {
@@ -41,23 +42,22 @@ k_ptable_tiled(const double* __restrict__ q, const double* __restrict__ qt,
         for (int j = 0; j < 4; ++j) acc[i][j] = comp[i][j] = 0.0;
 
     // this thread's staging slots: A rows (t/32 + 8 i) at l-offset t%32; B row t/64 + 4 i at
-    // column t%64
-    const int al = t & 31, ar = t >> 5;
-    const double* arow[8];
-    const double* aq[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t r = r0 + ar + 8 * i;
+    // column t%64.  Row offsets into q̃ and q are decoded once per CTA (−1: row past the end).
+    __shared__ int64_t row_qt[PT_BM];
+    __shared__ int row_q[PT_BM];
+    if (t < PT_BM) {
+        const int64_t r = r0 + t;
         if (r < R) {
             const int x = (int)(r % Nx);
             const int ab = (int)(r / Nx);
-            arow[i] = qt + ((int64_t)(ab % p) * Nx + x) * L;
-            aq[i] = q + (int64_t)(ab / p) * L;
+            row_qt[t] = ((int64_t)(ab % p) * Nx + x) * L;
+            row_q[t] = (ab / p) * L;
         } else {
-            arow[i] = nullptr;
-            aq[i] = nullptr;
+            row_qt[t] = -1;
+            row_q[t] = 0;
         }
     }
+    const int al = t & 31, ar = t >> 5;
     const int bc = t & 63, bl = t >> 6;
     const bool bok = m0 + bc < nmu;
 
@@ -69,8 +69,10 @@ k_ptable_tiled(const double* __restrict__ q, const double* __restrict__ qt,
             const double w = l < L ? lw[l] : 0.0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
+                const int64_t oq = row_qt[ar + 8 * i];
                 double v = 0.0;
-                if (l < L && arow[i]) v = __dmul_rn(__dmul_rn(w, aq[i][l]), arow[i][l]);
+                if (l < L && oq >= 0)
+                    v = __dmul_rn(__dmul_rn(w, q[row_q[ar + 8 * i] + l]), qt[oq + l]);
                 As[al][ar + 8 * i] = v;
             }
 #pragma unroll
@@ -112,54 +114,73 @@ k_ptable_tiled(const double* __restrict__ q, const double* __restrict__ qt,
 
 // ---- Γ cells --------------------------------------------------------------------------------
 // A CTA owns a 16 x 16 tile of (n, n') cells and one contiguous chunk of the radial points
-// (grid.z): for each x it stages P[:, :, x, μ-chunk] transposed ([μ][a*p+b], odd row stride) so
-// the nine operands of a cell's 3 x 3 matrix are read at (r_i, c_j) offsets of one short row,
-// sums the permanent against the μ rule, then adds w_x r_x² times that to the chunk's partial.
-// k_gamma2d_reduce adds the chunk partials in ascending x order (deterministic for a given
-// split) and applies 1/(48π).
+// (grid.z): for each x it stages P[:, :, x, μ-chunk] as [a*p+b][MC + 1] (odd row stride: lanes
+// that differ in (a, b) hit different banks, lanes that agree are a broadcast), so the nine
+// operands of a cell's 3 x 3 matrix sit at nine fixed per-thread row bases and the μ index is
+// an immediate offset in the unrolled loop.  The permanent is expanded along its first row
+// (3 mul + 5 fma instead of the reference's 12 mul + 5 add; Γ2d agrees to rounding, which is
+// all the reference claims for this engine), summed against the μ rule, and w_x r_x² times
+// that is added to the chunk's partial.  Shared-memory bandwidth bounds the kernel: ten 8-byte
+// reads per (cell, x, μ) against nine FP64 instructions.  k_gamma2d_reduce adds the chunk
+// partials in ascending x order (deterministic for a given split) and applies 1/(48π).
 constexpr int G2_TILE = 16;  // 16 x 16 cells per CTA
 
+template <int MC>
 __global__ void __launch_bounds__(G2_TILE* G2_TILE)
 k_gamma2d_cells(const double* __restrict__ P, const int* __restrict__ modes, int n, int p,
-                int Nx, int nmu, int mc, int ps, int xsplit, const double* __restrict__ mu_w,
+                int Nx, int nmu, int xsplit, const double* __restrict__ mu_w,
                 const double* __restrict__ wr2, double* __restrict__ partial) {
-    extern __shared__ double sp[];  // [mc][ps]
+    constexpr int MCP = MC + 1;
+    extern __shared__ double sp[];  // [p*p][MCP], then the μ weights of the chunk [MC]
+    const int pp = p * p;
+    double* sw = sp + (size_t)pp * MCP;
     const int tn = threadIdx.x / G2_TILE, tq = threadIdx.x % G2_TILE;
     const int nrow = blockIdx.y * G2_TILE + tn, ncol = blockIdx.x * G2_TILE + tq;
     const bool ok = nrow < n && ncol < n;
-    int o[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    if (ok) {
-        const int r[3] = {modes[3 * nrow], modes[3 * nrow + 1], modes[3 * nrow + 2]};
-        const int c[3] = {modes[3 * ncol], modes[3 * ncol + 1], modes[3 * ncol + 2]};
+    const double* s[9];
+    {
+        int r[3] = {0, 0, 0}, c[3] = {0, 0, 0};
+        if (ok) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                r[i] = modes[3 * nrow + i];
+                c[i] = modes[3 * ncol + i];
+            }
+        }
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) o[3 * i + j] = r[i] * p + c[j];
+            for (int j = 0; j < 3; ++j) s[3 * i + j] = sp + (r[i] * p + c[j]) * MCP;
     }
-    const int pp = p * p;
     const int xa = (int)((int64_t)Nx * blockIdx.z / xsplit);
     const int xb = (int)((int64_t)Nx * (blockIdx.z + 1) / xsplit);
     double acc = 0.0;
     for (int x = xa; x < xb; ++x) {
         double inner = 0.0;
-        for (int m0 = 0; m0 < nmu; m0 += mc) {
-            const int mn = min(mc, nmu - m0);
+        for (int m0 = 0; m0 < nmu; m0 += MC) {
+            const int mn = min(MC, nmu - m0);
             __syncthreads();
-            for (int e = threadIdx.x; e < pp * mn; e += blockDim.x) {
-                const int ab = e / mn, mm = e - ab * mn;
-                sp[mm * ps + ab] = P[((int64_t)ab * Nx + x) * nmu + m0 + mm];
+            // a short last chunk is zero-filled (its permanents vanish): the loop below runs
+            // in unrolled groups of 8
+            for (int e = threadIdx.x; e < pp * MC; e += blockDim.x) {
+                const int ab = e / MC, mm = e % MC;
+                sp[ab * MCP + mm] = mm < mn ? P[((int64_t)ab * Nx + x) * nmu + m0 + mm] : 0.0;
             }
+            for (int e = threadIdx.x; e < MC; e += blockDim.x)
+                sw[e] = e < mn ? mu_w[m0 + e] : 0.0;
             __syncthreads();
-            if (ok) {
-                const double* s = sp;
-                for (int mm = 0; mm < mn; ++mm, s += ps) {
-                    const double m00 = s[o[0]], m01 = s[o[1]], m02 = s[o[2]];
-                    const double m10 = s[o[3]], m11 = s[o[4]], m12 = s[o[5]];
-                    const double m20 = s[o[6]], m21 = s[o[7]], m22 = s[o[8]];
-                    // engine2d.py:101-109 term order
-                    const double per = m00 * m11 * m22 + m00 * m12 * m21 + m01 * m10 * m22 +
-                                       m01 * m12 * m20 + m02 * m10 * m21 + m02 * m11 * m20;
-                    inner += per * mu_w[m0 + mm];
+            constexpr int U = MC < 8 ? MC : 8;  // zero-filled up to the next multiple of U
+            for (int mb = 0; mb < mn; mb += U) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int mm = mb + u;
+                    const double m00 = s[0][mm], m01 = s[1][mm], m02 = s[2][mm];
+                    const double m10 = s[3][mm], m11 = s[4][mm], m12 = s[5][mm];
+                    const double m20 = s[6][mm], m21 = s[7][mm], m22 = s[8][mm];
+                    const double per = m00 * (m11 * m22 + m12 * m21) +
+                                       m01 * (m10 * m22 + m12 * m20) +
+                                       m02 * (m10 * m21 + m11 * m20);
+                    inner += per * sw[mm];
                 }
             }
         }
@@ -192,11 +213,11 @@ void ptable_dev(const double* q, const double* qt, const double* lw, const doubl
     MG_CUDA(cudaDeviceSynchronize());
 }
 
-// x chunks per cell tile: enough CTAs for ~4 per SM, at most one chunk per radial point and
-// at most 1 GiB of partials.
+// x chunks per cell tile: about 16 CTAs per SM in total (4 resident at a time, so the last
+// wave's idle tail stays small), at most one chunk per radial point and 1 GiB of partials.
 int gamma2d_xsplit(int n, int Nx) {
     const int64_t tiles = (int64_t)ceil_div(n, G2_TILE) * ceil_div(n, G2_TILE);
-    int64_t xs = (148 * 4 + tiles - 1) / tiles;
+    int64_t xs = (148 * 16 + tiles - 1) / tiles;
     xs = std::min<int64_t>(xs, Nx);
     xs = std::min<int64_t>(xs, std::max<int64_t>(1, (int64_t(1) << 27) / ((int64_t)n * n)));
     return (int)std::max<int64_t>(1, xs);
@@ -212,16 +233,26 @@ void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int N
     dg.alloc((size_t)n * n);
     const int xsplit = gamma2d_xsplit(n, Nx);
     dpart.alloc((size_t)xsplit * n * n);
-    const int ps = (p * p) | 1;
-    const int mc = std::max(1, std::min(std::min(64, nmu), 12288 / ps));
-    const size_t shm = (size_t)ps * mc * sizeof(double);
-    if (shm > 48 * 1024)
-        MG_CUDA(cudaFuncSetAttribute(k_gamma2d_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)shm));
     MG_REQUIRE(ceil_div(n, G2_TILE) <= 65535, "too many modes for the cell grid");
     dim3 grid(ceil_div(n, G2_TILE), ceil_div(n, G2_TILE), xsplit);
-    k_gamma2d_cells<<<grid, G2_TILE * G2_TILE, shm>>>(P_dev, dm.p, n, p, Nx, nmu, mc, ps, xsplit,
-                                                        dw.p, dr.p, dpart.p);
+    // μ chunk: the largest of 64 / 16 / 4 / 1 whose staged [p²][MC + 1] block fits 200 KB
+    auto launch = [&](auto mc_tag) {
+        constexpr int MC = decltype(mc_tag)::value;
+        const size_t shm = ((size_t)p * p * (MC + 1) + MC) * sizeof(double);
+        if (shm > 48 * 1024)
+            MG_CUDA(cudaFuncSetAttribute(k_gamma2d_cells<MC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        k_gamma2d_cells<MC><<<grid, G2_TILE * G2_TILE, shm>>>(P_dev, dm.p, n, p, Nx, nmu, xsplit,
+                                                                dw.p, dr.p, dpart.p);
+    };
+    const size_t cap = 200 * 1024 / sizeof(double), pp = (size_t)p * p;
+    if (pp * 65 + 64 <= cap) launch(std::integral_constant<int, 64>{});
+    else if (pp * 17 + 16 <= cap) launch(std::integral_constant<int, 16>{});
+    else if (pp * 5 + 4 <= cap) launch(std::integral_constant<int, 4>{});
+    else {
+        MG_REQUIRE(pp * 2 + 1 <= cap, "p_max too large for the 2D cell kernel");
+        launch(std::integral_constant<int, 1>{});
+    }
     MG_LAUNCHED();
     const int64_t cells = (int64_t)n * n;
     k_gamma2d_reduce<<<ceil_div(cells, 256), 256>>>(dpart.p, cells, xsplit, dg.p);
