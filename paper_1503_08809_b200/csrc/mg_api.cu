@@ -67,7 +67,8 @@ DeviceGuard::DeviceGuard(int device) {
 using namespace mg;
 
 template <class F>
-static int guarded(F&& f) {
+static int guarded_named(const char* name, F&& f) {
+    NvtxRange range(name);
     try {
         f();
         g_last_error.clear();
@@ -83,6 +84,9 @@ static int guarded(F&& f) {
         return MG_ECUDA;
     }
 }
+
+// every entry point: an NVTX range named after the C-ABI function around the guarded body
+#define guarded(...) guarded_named(__func__, __VA_ARGS__)
 
 static void full_range_bounds(const DomainIndex& D, int64_t begin, int64_t end, int* s, int* e) {
     MG_REQUIRE(0 <= begin && begin <= end && end <= D.count, "invalid flat range");

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -43,6 +44,19 @@ inline void check_cuda(cudaError_t e, const char* what, const char* file, int li
     do {                      \
         if (!(cond)) ::mg::fail(MG_EINVAL, (msg)); \
     } while (0)
+
+// NVTX range for the enclosing scope (header-only nvtx3: a no-op unless a tool such as nsys or
+// ncu --nvtx is attached).  Every C-ABI entry point opens one named after itself; the Γ
+// pipeline adds ranges for row preparation, each batch's enqueue and the final gather.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define MG_NVTX_CAT2(a, b) a##b
+#define MG_NVTX_CAT(a, b) MG_NVTX_CAT2(a, b)
+#define MG_NVTX(name) ::mg::NvtxRange MG_NVTX_CAT(mg_nvtx_, __LINE__)(name)
 
 // Selects `device` for the lifetime of the guard and verifies it is an sm_100 part.
 struct DeviceGuard {

@@ -1135,8 +1135,12 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
     const int pp = p * p;
     const int ncols = p * nm;
 
+    MG_NVTX("mg:run_pipeline");
     MgPrepared& pre = P->prep;
-    if (!pre.valid) prepare_batches(P, hrows, hzoff, st);
+    if (!pre.valid) {
+        MG_NVTX("mg:prepare_batches");
+        prepare_batches(P, hrows, hzoff, st);
+    }
     const std::vector<MgTile>& tiles = pre.tiles;
     const std::vector<int>& tile_first = pre.tile_first;
     const int max_tile_rows = pre.max_tile_rows;
@@ -1267,6 +1271,7 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         const Batch& B = batches[k];
         const int nb = (int)(B.e1 - B.b1);
         const int tf = tile_first[B.bidx], tl = tile_first[B.bidx + 1];
+        MG_NVTX("mg:batch_enqueue");
 #if MG_SIDE
         // side stream, once x(k-1) has consumed S: pair products of batch k (and, MG_SIDE 2,
         // the panels of batch k), beside the run contraction of batch k
@@ -2246,6 +2251,7 @@ void nonsep_collect(mg_plan* P) {
 // Resident sparse domain of the non-separable path: validated, packed (l1,l2,l3,0) int4 + W.
 void nonsep_set_domain(mg_plan* P, const int32_t* l1, const int32_t* l2, const int32_t* l3,
                        const double* W, int64_t count) {
+    MG_NVTX("mg:nonsep_set_domain");
     std::vector<int32_t> packed(4 * (size_t)count);
     for (int64_t i = 0; i < count; ++i) {
         MG_REQUIRE(l1[i] <= l2[i] && l2[i] <= l3[i], "triples must satisfy l1 <= l2 <= l3");
@@ -2272,6 +2278,7 @@ void nonsep_set_domain(mg_plan* P, const int32_t* l1, const int32_t* l2, const i
 // optional) and b_host (optional) receive the nm coefficients.
 void nonsep_execute(mg_plan* P, const double* alpha, double* b_dev, double* b_host,
                     cudaStream_t st) {
+    MG_NVTX("mg:nonsep_execute");
     const int nm = P->nm, p = P->p, P2 = P->P2;
     P->ns_b.ensure(nm);
     if (P->ns_count == 0) {

@@ -200,6 +200,7 @@ __global__ void k_gamma2d_reduce(const double* __restrict__ partial, int64_t cel
 
 void ptable_dev(const double* q, const double* qt, const double* lw, const double* leg, int p,
                 int Nx, int L, int nmu, double* P_dev) {
+    MG_NVTX("mg:ptable");
     DBuf<double> dq, dqt, dlw, dleg;
     dq.upload(q, (size_t)p * L);
     dqt.upload(qt, (size_t)p * Nx * L);
@@ -225,6 +226,7 @@ int gamma2d_xsplit(int n, int Nx) {
 
 void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int Nx, int nmu,
                  const double* mu_w, const double* wr2, double* gamma_host) {
+    MG_NVTX("mg:gamma2d_cells");
     DBuf<int> dm;
     DBuf<double> dw, dr, dg, dpart;
     dm.upload(modes_host, 3 * (size_t)n);

@@ -434,6 +434,7 @@ void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x
                       const double* eps, const double* qk, int p, int l_min, int l_max,
                       double X, double kd, double amp, double* C_dev, double* qt_dev,
                       double* delta_out_dev, cudaStream_t s) {
+    MG_NVTX("mg:build_qtilde");
     MG_REQUIRE(2 <= l_min && l_min <= l_max, "require 2 <= l_min <= l_max");
     MG_REQUIRE(Nk >= 1 && Nx >= 1 && p >= 1, "Nk, Nx, p must be >= 1");
     // the sweep kernel holds up to QB_PMAX components (4 DMMA m-fragments); larger bases are
