@@ -15,13 +15,16 @@ from __future__ import annotations
 
 import importlib
 
-__all__ = ["install", "uninstall", "gamma3d_matrix_shim", "gamma2d_matrix_shim"]
+__all__ = ["install", "uninstall", "gamma3d_matrix_shim", "gamma2d_matrix_shim",
+           "build_ptable_shim"]
 
 # (module, attribute) pairs the reference binds the two engines to
 _SITES_3D = (("", "gamma3d_matrix"), (".engine3d", "gamma3d_matrix"),
              (".harness", "gamma3d_matrix"))
 _SITES_2D = (("", "gamma2d_matrix"), (".engine2d", "gamma2d_matrix"),
              (".harness", "gamma2d_matrix"))
+# build_ptable (engine2d.py:62-95) is public too; gamma2d_matrix calls it through its module
+_SITES_PT = (("", "build_ptable"), (".engine2d", "build_ptable"))
 
 
 def _gm_class(cp):
@@ -61,12 +64,26 @@ def gamma2d_matrix_shim(cp):
     return gamma2d_matrix
 
 
+def build_ptable_shim(cp):
+    """A build_ptable with the reference signature (engine2d.py:62-64): the table is built on
+    the GPU (bit-identical) and returned as the reference's own PTable class."""
+    from .engine2d import DEFAULT_PTABLE_BUDGET, build_ptable as b200_build_ptable
+
+    PT = importlib.import_module(cp.__name__ + ".engine2d").PTable
+
+    def build_ptable(tables, grid, rule, legendre, budget_bytes=DEFAULT_PTABLE_BUDGET):
+        return PT(b200_build_ptable(tables, grid, rule, legendre, budget_bytes).values)
+    build_ptable.__wrapped_b200__ = True
+    return build_ptable
+
+
 def install(cp, engines=("3d", "2d"), setattr_fn=setattr):
     """Rebind the reference's engine names; returns the originals for `uninstall`.
     `setattr_fn` may be pytest's monkeypatch.setattr (automatic restore)."""
     saved = []
     for tag, sites, make in (("3d", _SITES_3D, gamma3d_matrix_shim),
-                             ("2d", _SITES_2D, gamma2d_matrix_shim)):
+                             ("2d", _SITES_2D, gamma2d_matrix_shim),
+                             ("2d", _SITES_PT, build_ptable_shim)):
         if tag not in engines:
             continue
         fn = make(cp)

@@ -148,6 +148,67 @@ class TestOrderedEnumeration:                              # test_engine3d.py:97
         assert relative_gap(ordered.values, unordered.values) < 1e-12
 
 
+class TestEngine2D:                                        # test_engine2d.py:50-135
+    """The reference's μ-engine tests with build_ptable / gamma2d_matrix rebound to the GPU;
+    gamma2d_entry, gamma2d_entry_naive and gamma2d_matrix_naive stay the reference's own."""
+
+    def test_ptable_shape_and_direct_sum(self, desk):                     # :51-65
+        from cmbproj.engine2d import PTable, _l_weight
+        assert getattr(cp.build_ptable, "__wrapped_b200__", False)
+        pt = cp.build_ptable(desk.tables, desk.grid, desk.rule, desk.legendre)
+        assert isinstance(pt, PTable)
+        assert pt.values.shape == (3, 3, len(desk.grid), desk.rule.n)
+        t = desk.tables
+        lw = _l_weight(t)
+        pl = desk.legendre[t.l_min:t.l_max + 1]
+        for a, b, x, m in [(0, 0, 0, 0), (1, 2, 10, 5), (2, 1, 53, 26)]:
+            direct = float(np.sum(lw * t.q[a] * t.q_tilde[b, x] * pl[:, m]))
+            assert pt.values[a, b, x, m] == pytest.approx(direct, rel=1e-12)
+
+    def test_ptable_budget_and_determinism(self, desk):                   # :67-75
+        with pytest.raises(MemoryError):
+            cp.build_ptable(desk.tables, desk.grid, desk.rule, desk.legendre, budget_bytes=1024)
+        a = cp.build_ptable(desk.tables, desk.grid, desk.rule, desk.legendre)
+        b = cp.build_ptable(desk.tables, desk.grid, desk.rule, desk.legendre)
+        assert np.array_equal(a.values, b.values)
+
+    @pytest.mark.parametrize("integrator", ["trap", "hermite", "spline"])
+    def test_reference_entries_from_gpu_table(self, desk, integrator):     # :79-97
+        pt = cp.build_ptable(desk.tables, desk.grid, desk.rule, desk.legendre)
+        for n, n_prime in [(0, 0), (0, 5), (3, 7), (9, 2)]:
+            fast = cp.gamma2d_entry(n, n_prime, pt, desk.mapping, desk.grid, desk.rule,
+                                    integrator=integrator)
+            naive = cp.gamma2d_entry_naive(n, n_prime, desk.tables, desk.mapping, desk.grid,
+                                           desk.rule, desk.legendre, integrator=integrator)
+            assert fast == pytest.approx(naive, rel=1e-12)
+
+    def test_matrix_vs_naive_matrix(self, desk):                          # :110-116
+        fast = cp.gamma2d_matrix(desk.tables, desk.mapping, desk.grid, desk.rule, desk.legendre)
+        naive = cp.gamma2d_matrix_naive(desk.tables, desk.mapping, desk.grid, desk.rule,
+                                        desk.legendre)
+        assert relative_gap(fast.values, naive.values) < 1e-12
+        assert np.isfinite(fast.values).all() and np.any(fast.values != 0.0)
+
+    @pytest.mark.parametrize("workers", [2, 3, 5])
+    def test_bitwise_identical_across_workers(self, desk, workers):       # :118-123
+        base = cp.gamma2d_matrix(desk.tables, desk.mapping, desk.grid, desk.rule, desk.legendre,
+                                 workers=1)
+        multi = cp.gamma2d_matrix(desk.tables, desk.mapping, desk.grid, desk.rule,
+                                  desk.legendre, workers=workers)
+        assert np.array_equal(base.values, multi.values)
+
+    def test_meta_and_reference_ptable_argument(self, desk):              # :125-131
+        g = cp.gamma2d_matrix(desk.tables, desk.mapping, desk.grid, desk.rule, desk.legendre,
+                              workers=2)
+        assert g.meta["engine"] == "modal2d" and g.meta["workers"] == 2
+        assert g.meta["n_mu"] == desk.rule.n
+        assert g.meta["tables"] == desk.tables.fingerprint()
+        pt = cp.build_ptable(desk.tables, desk.grid, desk.rule, desk.legendre)
+        again = cp.gamma2d_matrix(desk.tables, desk.mapping, desk.grid, desk.rule,
+                                  desk.legendre, ptable=pt)
+        assert np.array_equal(again.values, g.values)
+
+
 class TestAcceptance:
     def test_criterion_1_separable_direct_equivalence(self, accept):   # :50-57
         g2 = cp.gamma2d_matrix(accept.tables, accept.mapping, accept.grid, accept.rule,
