@@ -9,10 +9,12 @@
 // Kahan update y = term - comp; t = acc + y; comp = (t - acc) - y), each FP64 op an explicit
 // round-to-nearest intrinsic, so it reproduces the reference table bit for bit.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
 #include "mg_common.cuh"
+#include "mg_dmma.cuh"
 
 namespace mg {
 
@@ -198,6 +200,159 @@ __global__ void k_gamma2d_reduce(const double* __restrict__ partial, int64_t cel
     gamma[i] = acc / (48.0 * 3.141592653589793);
 }
 
+// ---- Γ cells on the FP64 tensor pipe (p ≤ 8) -------------------------------------------------
+// The permanent splits along its last row:  perm = Σ_k P[r2,c_k] · V[(r0,r1)][(c_i,c_j)]  with
+// V[(a,b)][(c,d)] = P[a,c]P[b,d] + P[a,d]P[b,c]  ((i,j) the two columns other than k), so with
+// the sample index s = (x, μ) and W_s = w_x r_x² w_μ
+//     D[(a,c)][(a'≤b'),(c'≤d')] = Σ_s P_s[a,c] · W_s V_s[(a',b')][(c',d')]
+// is one GEMM — M = p² rows, N = (p(p+1)/2)² columns, K = Nx·n_μ — and every cell is three
+// entries of D.  It costs about as many FLOPs as the per-cell form (p⁶/2 against 10·p⁶/36 FP64
+// instructions per sample) but runs them as DMMA.8x8x4 with ~0.9 shared-memory reads per DMMA
+// instead of ten per cell-sample, which is what bounded k_gamma2d_cells.  A CTA (8 warps) owns
+// 24 n-fragments and a contiguous range of samples (split-K, partials reduced in order by
+// k_gamma2d_gather); P_s chunks of 64 samples are double-buffered through shared memory with
+// 8-byte cp.async; the B operand is never stored: a lane forms its element from four P reads.
+constexpr int G2D_KC = 64;           // samples per stage
+constexpr int G2D_LD = G2D_KC + 4;   // row stride: fragment reads (row g, sample t) conflict-free
+constexpr int G2D_FN = 3;            // n-fragments per warp
+constexpr int G2D_WARPS = 8;
+
+__host__ __device__ inline int g2d_pair(int a, int b) { return b * (b + 1) / 2 + a; }  // a <= b
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(src_bytes));
+}
+
+template <int MF>
+__global__ void __launch_bounds__(G2D_WARPS * 32, 1)
+k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
+               const double* __restrict__ mu_w, int p, int nmu, int64_t S, int nchunks,
+               int N, int Npad, double* __restrict__ Dpart) {
+    extern __shared__ double sm[];
+    constexpr int ROWS = MF * 8;
+    double* Ps = sm;                               // [2][ROWS][G2D_LD]
+    double* Ws = sm + 2 * ROWS * G2D_LD;           // [2][G2D_KC]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int pp = p * p, P2 = p * (p + 1) / 2;
+    // this lane's B columns: n = (a'<=b', c'<=d') -> four row offsets into the staged P block
+    const int nf0 = (blockIdx.x * G2D_WARPS + warp) * G2D_FN;
+    int o[G2D_FN][4];
+    double vm[G2D_FN];
+#pragma unroll
+    for (int f = 0; f < G2D_FN; ++f) {
+        const int n = (nf0 + f) * 8 + g;
+        vm[f] = n < N ? 1.0 : 0.0;
+        int ab = n < N ? n / P2 : 0, cd = n < N ? n % P2 : 0;
+        int b = 0, d = 0;
+        while (g2d_pair(0, b + 1) <= ab) ++b;
+        while (g2d_pair(0, d + 1) <= cd) ++d;
+        const int a = ab - g2d_pair(0, b), c = cd - g2d_pair(0, d);
+        o[f][0] = (a * p + c) * G2D_LD;
+        o[f][1] = (b * p + d) * G2D_LD;
+        o[f][2] = (a * p + d) * G2D_LD;
+        o[f][3] = (b * p + c) * G2D_LD;
+    }
+    const bool warp_live = nf0 * 8 < N;
+    // sample chunks of this CTA
+    const int c0 = (int)((int64_t)nchunks * blockIdx.y / gridDim.y);
+    const int c1 = (int)((int64_t)nchunks * (blockIdx.y + 1) / gridDim.y);
+    // padding rows (pp <= row < ROWS) stay zero in both buffers
+    for (int e = tid; e < 2 * ROWS * G2D_LD; e += blockDim.x)
+        if ((e / G2D_LD) % ROWS >= pp) Ps[e] = 0.0;
+
+    auto stage = [&](int ch, int buf) {
+        const int64_t s0 = (int64_t)ch * G2D_KC;
+        double* dst = Ps + buf * ROWS * G2D_LD;
+        for (int e = tid; e < pp * G2D_KC; e += blockDim.x) {
+            const int row = e / G2D_KC, k = e % G2D_KC;
+            const int64_t sidx = s0 + k;
+            const bool ok = sidx < S;
+            cp_async8(dst + row * G2D_LD + k, ok ? P + (int64_t)row * S + sidx : P, ok ? 8 : 0);
+        }
+        if (tid < G2D_KC) {
+            const int64_t sidx = s0 + tid;
+            Ws[buf * G2D_KC + tid] =
+                sidx < S ? wr2[sidx / nmu] * mu_w[sidx % nmu] : 0.0;
+        }
+        cp_async_commit();
+    };
+
+    double acc[MF][G2D_FN][2];
+#pragma unroll
+    for (int m = 0; m < MF; ++m)
+#pragma unroll
+        for (int f = 0; f < G2D_FN; ++f) acc[m][f][0] = acc[m][f][1] = 0.0;
+
+    if (c0 < c1) stage(c0, 0);
+    for (int ch = c0; ch < c1; ++ch) {
+        const int buf = (ch - c0) & 1;
+        if (ch + 1 < c1) {
+            stage(ch + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        if (warp_live) {
+            const double* ps = Ps + buf * ROWS * G2D_LD;
+            const double* ws = Ws + buf * G2D_KC;
+#pragma unroll 4
+            for (int k = t; k < G2D_KC; k += 4) {
+                const double w = ws[k];
+                double b[G2D_FN];
+#pragma unroll
+                for (int f = 0; f < G2D_FN; ++f)
+                    b[f] = (w * vm[f]) * (ps[o[f][0] + k] * ps[o[f][1] + k] +
+                                          ps[o[f][2] + k] * ps[o[f][3] + k]);
+#pragma unroll
+                for (int m = 0; m < MF; ++m) {
+                    const double a = ps[(m * 8 + g) * G2D_LD + k];
+#pragma unroll
+                    for (int f = 0; f < G2D_FN; ++f) dmma884(acc[m][f], a, b[f]);
+                }
+            }
+        }
+        __syncthreads();  // the next iteration's stage() overwrites the other buffer
+    }
+    if (!warp_live) return;
+    double* out = Dpart + (int64_t)blockIdx.y * ROWS * Npad;
+#pragma unroll
+    for (int m = 0; m < MF; ++m)
+#pragma unroll
+        for (int f = 0; f < G2D_FN; ++f) {
+            const int col = (nf0 + f) * 8 + 2 * t;
+            if (col < Npad) {
+                out[(int64_t)(m * 8 + g) * Npad + col] = acc[m][f][0];
+                out[(int64_t)(m * 8 + g) * Npad + col + 1] = acc[m][f][1];
+            }
+        }
+}
+
+// Γ2d[n,n'] = Σ_k D[(r2,c_k)][(r0,r1),(c_i,c_j)] / 48π, D summed over the split-K partials in
+// ascending order (deterministic).
+__global__ void k_gamma2d_gather(const double* __restrict__ Dpart, int ksplit, int rows, int Npad,
+                                 const int* __restrict__ modes, int n, int p,
+                                 double* __restrict__ gamma) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * n) return;
+    const int nr = (int)(i / n), nc = (int)(i % n);
+    const int r0 = modes[3 * nr], r1 = modes[3 * nr + 1], r2 = modes[3 * nr + 2];
+    const int c[3] = {modes[3 * nc], modes[3 * nc + 1], modes[3 * nc + 2]};
+    const int P2 = p * (p + 1) / 2;
+    const int ab = g2d_pair(r0, r1);
+    // columns other than k, in ascending order (the mapping keeps i <= j <= k)
+    const int64_t e0 = (int64_t)(r2 * p + c[0]) * Npad + ab * P2 + g2d_pair(c[1], c[2]);
+    const int64_t e1 = (int64_t)(r2 * p + c[1]) * Npad + ab * P2 + g2d_pair(c[0], c[2]);
+    const int64_t e2 = (int64_t)(r2 * p + c[2]) * Npad + ab * P2 + g2d_pair(c[0], c[1]);
+    double acc = 0.0;
+    for (int z = 0; z < ksplit; ++z) {
+        const double* D = Dpart + (int64_t)z * rows * Npad;
+        acc += (D[e0] + D[e1]) + D[e2];
+    }
+    gamma[i] = acc / (48.0 * 3.141592653589793);
+}
+
 void ptable_dev(const double* q, const double* qt, const double* lw, const double* leg, int p,
                 int Nx, int L, int nmu, double* P_dev) {
     MG_NVTX("mg:ptable");
@@ -224,6 +379,42 @@ int gamma2d_xsplit(int n, int Nx) {
     return (int)std::max<int64_t>(1, xs);
 }
 
+static void gamma2d_dmma(const double* P_dev, const int* modes_dev, int n, int p, int Nx, int nmu,
+                         const double* mu_w_dev, const double* wr2_dev, double* gamma_dev) {
+    const int P2 = p * (p + 1) / 2, N = P2 * P2, Npad = (int)round_up(N, 8);
+    const int MF = ceil_div(p * p, 8), rows = MF * 8;
+    const int64_t S = (int64_t)Nx * nmu;
+    const int nchunks = ceil_div(S, G2D_KC);
+    const int gx = ceil_div(Npad / 8, G2D_FN * G2D_WARPS);
+    // one CTA per SM in total, at least 4 chunks per CTA
+    const int ksplit = std::max(1, std::min(std::max(148 / gx, 1), std::max(nchunks / 4, 1)));
+    DBuf<double> dpart((size_t)ksplit * rows * Npad);
+    const size_t shm = ((size_t)2 * rows * G2D_LD + 2 * G2D_KC) * sizeof(double);
+    dim3 grid(gx, ksplit);
+    auto launch = [&](auto mf_tag) {
+        constexpr int MFc = decltype(mf_tag)::value;
+        MG_CUDA(cudaFuncSetAttribute(k_gamma2d_dmma<MFc>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        k_gamma2d_dmma<MFc><<<grid, G2D_WARPS * 32, shm>>>(P_dev, wr2_dev, mu_w_dev, p, nmu, S,
+                                                            nchunks, N, Npad, dpart.p);
+    };
+    switch (MF) {
+        case 1: launch(std::integral_constant<int, 1>{}); break;
+        case 2: launch(std::integral_constant<int, 2>{}); break;
+        case 3: launch(std::integral_constant<int, 3>{}); break;
+        case 4: launch(std::integral_constant<int, 4>{}); break;
+        case 5: launch(std::integral_constant<int, 5>{}); break;
+        case 6: launch(std::integral_constant<int, 6>{}); break;
+        case 7: launch(std::integral_constant<int, 7>{}); break;
+        default: launch(std::integral_constant<int, 8>{}); break;
+    }
+    MG_LAUNCHED();
+    const int64_t cells = (int64_t)n * n;
+    k_gamma2d_gather<<<ceil_div(cells, 256), 256>>>(dpart.p, ksplit, rows, Npad, modes_dev, n, p,
+                                                      gamma_dev);
+    MG_LAUNCHED();
+}
+
 void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int Nx, int nmu,
                  const double* mu_w, const double* wr2, double* gamma_host) {
     MG_NVTX("mg:gamma2d_cells");
@@ -233,32 +424,37 @@ void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int N
     dw.upload(mu_w, nmu);
     dr.upload(wr2, Nx);
     dg.alloc((size_t)n * n);
-    const int xsplit = gamma2d_xsplit(n, Nx);
-    dpart.alloc((size_t)xsplit * n * n);
-    MG_REQUIRE(ceil_div(n, G2_TILE) <= 65535, "too many modes for the cell grid");
-    dim3 grid(ceil_div(n, G2_TILE), ceil_div(n, G2_TILE), xsplit);
-    // μ chunk: the largest of 64 / 16 / 4 / 1 whose staged [p²][MC + 1] block fits 200 KB
-    auto launch = [&](auto mc_tag) {
-        constexpr int MC = decltype(mc_tag)::value;
-        const size_t shm = ((size_t)p * p * (MC + 1) + MC) * sizeof(double);
-        if (shm > 48 * 1024)
-            MG_CUDA(cudaFuncSetAttribute(k_gamma2d_cells<MC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        k_gamma2d_cells<MC><<<grid, G2_TILE * G2_TILE, shm>>>(P_dev, dm.p, n, p, Nx, nmu, xsplit,
-                                                                dw.p, dr.p, dpart.p);
-    };
-    const size_t cap = 200 * 1024 / sizeof(double), pp = (size_t)p * p;
-    if (pp * 65 + 64 <= cap) launch(std::integral_constant<int, 64>{});
-    else if (pp * 17 + 16 <= cap) launch(std::integral_constant<int, 16>{});
-    else if (pp * 5 + 4 <= cap) launch(std::integral_constant<int, 4>{});
-    else {
-        MG_REQUIRE(pp * 2 + 1 <= cap, "p_max too large for the 2D cell kernel");
-        launch(std::integral_constant<int, 1>{});
+    const bool force_lds = std::getenv("MG_G2D_LDS") != nullptr;  // A/B switch (read per call)
+    if (p <= 8 && !force_lds) {
+        gamma2d_dmma(P_dev, dm.p, n, p, Nx, nmu, dw.p, dr.p, dg.p);
+    } else {
+        const int xsplit = gamma2d_xsplit(n, Nx);
+        dpart.alloc((size_t)xsplit * n * n);
+        MG_REQUIRE(ceil_div(n, G2_TILE) <= 65535, "too many modes for the cell grid");
+        dim3 grid(ceil_div(n, G2_TILE), ceil_div(n, G2_TILE), xsplit);
+        // μ chunk: the largest of 64 / 16 / 4 / 1 whose staged [p²][MC + 1] block fits 200 KB
+        auto launch = [&](auto mc_tag) {
+            constexpr int MC = decltype(mc_tag)::value;
+            const size_t shm = ((size_t)p * p * (MC + 1) + MC) * sizeof(double);
+            if (shm > 48 * 1024)
+                MG_CUDA(cudaFuncSetAttribute(k_gamma2d_cells<MC>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+            k_gamma2d_cells<MC><<<grid, G2_TILE * G2_TILE, shm>>>(P_dev, dm.p, n, p, Nx, nmu, xsplit,
+                                                                    dw.p, dr.p, dpart.p);
+        };
+        const size_t cap = 200 * 1024 / sizeof(double), pp = (size_t)p * p;
+        if (pp * 65 + 64 <= cap) launch(std::integral_constant<int, 64>{});
+        else if (pp * 17 + 16 <= cap) launch(std::integral_constant<int, 16>{});
+        else if (pp * 5 + 4 <= cap) launch(std::integral_constant<int, 4>{});
+        else {
+            MG_REQUIRE(pp * 2 + 1 <= cap, "p_max too large for the 2D cell kernel");
+            launch(std::integral_constant<int, 1>{});
+        }
+        MG_LAUNCHED();
+        const int64_t cells = (int64_t)n * n;
+        k_gamma2d_reduce<<<ceil_div(cells, 256), 256>>>(dpart.p, cells, xsplit, dg.p);
+        MG_LAUNCHED();
     }
-    MG_LAUNCHED();
-    const int64_t cells = (int64_t)n * n;
-    k_gamma2d_reduce<<<ceil_div(cells, 256), 256>>>(dpart.p, cells, xsplit, dg.p);
-    MG_LAUNCHED();
     MG_CUDA(cudaMemcpy(gamma_host, dg.p, (size_t)n * n * sizeof(double),
                        cudaMemcpyDeviceToHost));
 }

@@ -331,14 +331,25 @@ class TestGamma2D:
         g3 = gamma3d_matrix(t, m, r, h2_mode="exact").values
         assert gap_rel(got.values, g3) < 1e-10
 
+    @pytest.mark.parametrize("lds", [False, True])
     @pytest.mark.parametrize("lmin,lmax,p,nx,nmu", [(2, 70, 5, 37, 107),    # 3 l chunks, 2 μ tiles
                                                      (3, 34, 7, 19, 65),     # 33 = 32 + 1 rows of l
-                                                     (2, 150, 3, 130, 228)])  # 19 row tiles
-    def test_tiled_kernels_vs_oracle(self, lmin, lmax, p, nx, nmu):
+                                                     (2, 150, 3, 130, 228),  # 19 row tiles
+                                                     (2, 30, 8, 23, 50),     # p = 8: 8 m-fragments
+                                                     (2, 24, 9, 11, 40),     # p > 8: per-cell form
+                                                     (2, 12, 1, 5, 20),      # one mode
+                                                     (2, 40, 2, 9, 64)])
+    def test_tiled_kernels_vs_oracle(self, lmin, lmax, p, nx, nmu, lds, monkeypatch):
         """Sizes that cross every tile edge of the P-table kernel (64 x 64 x 32: partial row,
-        column and l tiles) and of the cell kernel (x chunks per CTA, μ chunks of 64, partial
-        16 x 16 cell tiles) against oracle/gamma2d_ref.py (pinned to the reference's tables)."""
+        column and l tiles) and of both cell kernels — the DMMA form (p <= 8: partial
+        m-fragments, partial n-fragments, idle warps, split-K with a short last chunk) and the
+        per-cell form (MG_G2D_LDS=1 or p > 8: x chunks per CTA, μ chunks of 64, partial 16 x 16
+        cell tiles) — against oracle/gamma2d_ref.py (pinned to the reference's tables)."""
         from oracle import gamma2d_ref
+        if lds:
+            monkeypatch.setenv("MG_G2D_LDS", "1")
+        else:
+            monkeypatch.delenv("MG_G2D_LDS", raising=False)
         from paper_1503_08809_b200 import (build_ptable, default_mode_mapping, gamma2d_matrix,
                                            gauss_legendre, legendre_table)
         t, r = TestEdgeCases().random_tables(lmin, lmax, p, nx, seed=11)
