@@ -212,11 +212,11 @@ __global__ void k_gamma2d_reduce(const double* __restrict__ partial, int64_t cel
 // 24 n-fragments and a contiguous range of samples (split-K, partials reduced in order by
 // k_gamma2d_gather); P_s chunks of 64 samples are double-buffered through shared memory with
 // 8-byte cp.async; the B operand is never stored: a lane forms its element from four P reads.
-constexpr int G2D_KC = 64;           // samples per stage
-constexpr int G2D_LD = G2D_KC + 4;   // row stride: fragment reads (row g, sample t) conflict-free
-constexpr int G2D_FN = 3;            // n-fragments per warp
-constexpr int G2D_WARPS = 8;
-
+// Tile: WARPS warps of FN n-fragments each, KC samples per stage, row stride KC + 4 (fragment
+// reads of (row g, sample t) are then bank-conflict free).  Measured (profiles/r02_2d_engine.txt):
+// 12 warps x 2 fragments x 128 samples is fastest at p = 7, 8 (7-8 m-fragments feed 14-16 DMMAs
+// per operand pair), 16 warps x 2 x 128 below that, where a warp has less tensor work per
+// operand and more warps hide its loads.
 __host__ __device__ inline int g2d_pair(int a, int b) { return b * (b + 1) / 2 + a; }  // a <= b
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
@@ -224,13 +224,13 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_by
                  "r"(src_bytes));
 }
 
-template <int MF>
+template <int MF, int G2D_WARPS, int G2D_FN, int G2D_KC>
 __global__ void __launch_bounds__(G2D_WARPS * 32, 1)
 k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
                const double* __restrict__ mu_w, int p, int nmu, int64_t S, int nchunks,
                int N, int Npad, double* __restrict__ Dpart) {
     extern __shared__ double sm[];
-    constexpr int ROWS = MF * 8;
+    constexpr int ROWS = MF * 8, G2D_LD = G2D_KC + 4;
     double* Ps = sm;                               // [2][ROWS][G2D_LD]
     double* Ws = sm + 2 * ROWS * G2D_LD;           // [2][G2D_KC]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -261,20 +261,24 @@ k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
     for (int e = tid; e < 2 * ROWS * G2D_LD; e += blockDim.x)
         if ((e / G2D_LD) % ROWS >= pp) Ps[e] = 0.0;
 
+    // staging: a thread copies one sample column k of rows kr, kr + RSTEP, ... (8-byte cp.async,
+    // zero-filled past the last sample), so a chunk costs it one copy and two adds per element
+    constexpr int RSTEP = G2D_WARPS * 32 / G2D_KC;
+    static_assert(G2D_WARPS * 32 % G2D_KC == 0, "threads must tile the sample columns");
+    const int kcol = tid % G2D_KC, kr = tid / G2D_KC;
     auto stage = [&](int ch, int buf) {
-        const int64_t s0 = (int64_t)ch * G2D_KC;
-        double* dst = Ps + buf * ROWS * G2D_LD;
-        for (int e = tid; e < pp * G2D_KC; e += blockDim.x) {
-            const int row = e / G2D_KC, k = e % G2D_KC;
-            const int64_t sidx = s0 + k;
-            const bool ok = sidx < S;
-            cp_async8(dst + row * G2D_LD + k, ok ? P + (int64_t)row * S + sidx : P, ok ? 8 : 0);
+        const int64_t sidx = (int64_t)ch * G2D_KC + kcol;
+        const bool ok = sidx < S;
+        const double* src = ok ? P + (int64_t)kr * S + sidx : P;
+        double* dst = Ps + buf * ROWS * G2D_LD + kr * G2D_LD + kcol;
+        const int64_t sstep = ok ? (int64_t)RSTEP * S : 0;
+        const int bytes = ok ? 8 : 0;
+        for (int row = kr; row < pp; row += RSTEP) {
+            cp_async8(dst, src, bytes);
+            src += sstep;
+            dst += RSTEP * G2D_LD;
         }
-        if (tid < G2D_KC) {
-            const int64_t sidx = s0 + tid;
-            Ws[buf * G2D_KC + tid] =
-                sidx < S ? wr2[sidx / nmu] * mu_w[sidx % nmu] : 0.0;
-        }
+        if (kr == 0) Ws[buf * G2D_KC + kcol] = ok ? wr2[sidx / nmu] * mu_w[sidx % nmu] : 0.0;
         cp_async_commit();
     };
 
@@ -379,40 +383,43 @@ int gamma2d_xsplit(int n, int Nx) {
     return (int)std::max<int64_t>(1, xs);
 }
 
-static void gamma2d_dmma(const double* P_dev, const int* modes_dev, int n, int p, int Nx, int nmu,
-                         const double* mu_w_dev, const double* wr2_dev, double* gamma_dev) {
+template <int MF, int WARPS, int FN, int KC>
+static void launch_gamma2d_dmma(const double* P_dev, const int* modes_dev, int n, int p, int Nx,
+                                int nmu, const double* mu_w_dev, const double* wr2_dev,
+                                double* gamma_dev) {
     const int P2 = p * (p + 1) / 2, N = P2 * P2, Npad = (int)round_up(N, 8);
-    const int MF = ceil_div(p * p, 8), rows = MF * 8;
+    constexpr int rows = MF * 8, LD = KC + 4;
     const int64_t S = (int64_t)Nx * nmu;
-    const int nchunks = ceil_div(S, G2D_KC);
-    const int gx = ceil_div(Npad / 8, G2D_FN * G2D_WARPS);
+    const int nchunks = ceil_div(S, KC);
+    const int gx = ceil_div(Npad / 8, FN * WARPS);
     // one CTA per SM in total, at least 4 chunks per CTA
     const int ksplit = std::max(1, std::min(std::max(148 / gx, 1), std::max(nchunks / 4, 1)));
     DBuf<double> dpart((size_t)ksplit * rows * Npad);
-    const size_t shm = ((size_t)2 * rows * G2D_LD + 2 * G2D_KC) * sizeof(double);
-    dim3 grid(gx, ksplit);
-    auto launch = [&](auto mf_tag) {
-        constexpr int MFc = decltype(mf_tag)::value;
-        MG_CUDA(cudaFuncSetAttribute(k_gamma2d_dmma<MFc>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        k_gamma2d_dmma<MFc><<<grid, G2D_WARPS * 32, shm>>>(P_dev, wr2_dev, mu_w_dev, p, nmu, S,
-                                                            nchunks, N, Npad, dpart.p);
-    };
-    switch (MF) {
-        case 1: launch(std::integral_constant<int, 1>{}); break;
-        case 2: launch(std::integral_constant<int, 2>{}); break;
-        case 3: launch(std::integral_constant<int, 3>{}); break;
-        case 4: launch(std::integral_constant<int, 4>{}); break;
-        case 5: launch(std::integral_constant<int, 5>{}); break;
-        case 6: launch(std::integral_constant<int, 6>{}); break;
-        case 7: launch(std::integral_constant<int, 7>{}); break;
-        default: launch(std::integral_constant<int, 8>{}); break;
-    }
+    const size_t shm = ((size_t)2 * rows * LD + 2 * KC) * sizeof(double);
+    MG_CUDA(cudaFuncSetAttribute(k_gamma2d_dmma<MF, WARPS, FN, KC>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    k_gamma2d_dmma<MF, WARPS, FN, KC><<<dim3(gx, ksplit), WARPS * 32, shm>>>(
+        P_dev, wr2_dev, mu_w_dev, p, nmu, S, nchunks, N, Npad, dpart.p);
     MG_LAUNCHED();
     const int64_t cells = (int64_t)n * n;
     k_gamma2d_gather<<<ceil_div(cells, 256), 256>>>(dpart.p, ksplit, rows, Npad, modes_dev, n, p,
                                                       gamma_dev);
     MG_LAUNCHED();
+}
+
+static void gamma2d_dmma(const double* P_dev, const int* modes_dev, int n, int p, int Nx, int nmu,
+                         const double* mu_w_dev, const double* wr2_dev, double* gamma_dev) {
+#define MG_G2D_CASE(MF, W)                                                                    \
+    case MF:                                                                                  \
+        launch_gamma2d_dmma<MF, W, 2, 128>(P_dev, modes_dev, n, p, Nx, nmu, mu_w_dev, wr2_dev, \
+                                           gamma_dev);                                        \
+        break;
+    switch (ceil_div(p * p, 8)) {  // m-fragments: p = 1..8 -> 1, 1, 2, 2, 4, 5, 7, 8
+        MG_G2D_CASE(1, 16) MG_G2D_CASE(2, 16) MG_G2D_CASE(4, 16) MG_G2D_CASE(5, 16)
+        MG_G2D_CASE(7, 12) MG_G2D_CASE(8, 12)
+        default: fail(MG_EINVAL, "gamma2d_dmma: p must be <= 8");
+    }
+#undef MG_G2D_CASE
 }
 
 void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int Nx, int nmu,
