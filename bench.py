@@ -312,6 +312,115 @@ def run_nonsep(args):
     print(json.dumps(line), flush=True)
 
 
+def run_2d(args):
+    """`--config 2d`: the μ-quadrature engine (engine2d.py:62-211) at
+    l_max 512 / p 8 / Nx 300 (771 μ nodes, 120 modes).  A step is one Γ2d: the Kahan P table
+    plus the cell sums.  `value` = kernel time (CUDA events around the launches inside the
+    library, inputs already uploaded); `e2e` = the drop-in gamma2d_matrix call with host
+    buffers; `cpu_baseline` = the NumPy restatement on a subset of the radial points, against
+    which the GPU result on the same subset is checked."""
+    import torch
+
+    from paper_1503_08809_b200 import (BasisTables, RadialGrid, default_mode_mapping,
+                                       gamma2d_matrix, gauss_legendre, legendre_table,
+                                       shifted_legendre)
+    from paper_1503_08809_b200.engine2d import default_mu_points, last_kernel_ms
+    from paper_1503_08809_b200.quadrature import x_weights
+
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    lmin, lmax, p, nx = 2, 512, 8, 300
+    rng = np.random.default_rng(2015)
+    L = lmax - lmin + 1
+    ells = np.arange(lmin, lmax + 1, dtype=np.float64)
+    tables = BasisTables(shifted_legendre(p, lmin, lmax), rng.standard_normal((p, nx, L)) * 1e-3,
+                         rng.uniform(0.5, 2.0, L) * 1e-3, (2.0 * ells + 1.0) ** (1.0 / 6.0),
+                         lmin, lmax)
+    grid = RadialGrid(np.linspace(13000.0, 14500.0, nx))
+    mapping = default_mode_mapping(p)
+    rule = gauss_legendre(default_mu_points(lmax))
+    leg = legendre_table(lmax, rule)
+    n, nmu = mapping.n_max, rule.n
+    U = n * n * nx * nmu
+    P2 = p * (p + 1) // 2
+    ops_pt = 5.0 * p * p * nx * nmu * L                    # 1 mul + 4 Kahan add/sub, no FMA
+    flops_cells = 2.0 * p * p * P2 * P2 * nx * nmu         # the DMMA GEMM (p <= 8)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        g = gamma2d_matrix(tables, mapping, grid, rule, leg, device=local)
+    pt_ms, cell_ms, e2e = [], [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g = gamma2d_matrix(tables, mapping, grid, rule, leg, device=local)
+            e2e.append(time.perf_counter() - t0)
+            a, b = last_kernel_ms()
+            pt_ms.append(a)
+            cell_ms.append(b)
+    ms = float(np.mean(pt_ms) + np.mean(cell_ms))
+    e2e_s = float(np.median(e2e))
+    k_pt, k_cell = float(np.mean(pt_ms)), float(np.mean(cell_ms))
+    h2d = sum(x.nbytes for x in (tables.q, tables.q_tilde, tables.C, tables.v, leg[lmin:],
+                                 rule.weights, mapping.entries)) + nx * 8
+    if k_pt >= k_cell:
+        roof = {"bound": "tensor", "kernel": "k_ptable_tiled",
+                "achieved": ops_pt / (k_pt / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS / 2,
+                "unit": "TFLOP/s",
+                "note": "FP64 pipe, not the tensor cores: 5 individually rounded operations per "
+                        "(element, l) (1 mul + 4 Kahan add/sub; fusing any would break the "
+                        "bit-identical table), peak = the pipe's instruction rate = DFMA peak / 2"}
+    else:
+        roof = {"bound": "tensor", "kernel": "k_gamma2d_dmma", "achieved":
+                flops_cells / (k_cell / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "note": "cell sum as a DMMA.8x8x4 GEMM, M = p², N = (p(p+1)/2)², K = Nx·nμ"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel_ms_per_step"] = {"ptable": k_pt, "cells": k_cell}
+    roof["cells_tflops"] = flops_cells / (k_cell / 1e3) / 1e12
+    roof["ptable_tops"] = ops_pt / (k_pt / 1e3) / 1e12
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import gamma2d_ref
+        xs = np.unique(np.linspace(0, nx - 1, 24).astype(int))
+        sub = BasisTables(tables.q, np.ascontiguousarray(tables.q_tilde[:, xs]), tables.C,
+                          tables.v, lmin, lmax)
+        subgrid = RadialGrid(grid.r[xs])
+        wr2 = x_weights(subgrid.r)
+        t0 = time.perf_counter()
+        Pc = gamma2d_ref.ptable(sub.q, sub.q_tilde, sub.C, sub.v, lmin, lmax, leg)
+        want = gamma2d_ref.gamma2d(Pc, mapping.entries, rule.weights, wr2)
+        dt = time.perf_counter() - t0
+        got = gamma2d_matrix(sub, mapping, subgrid, rule, leg, device=local).values
+        err = float(np.max(np.abs(got - want)) / np.max(np.abs(want)))
+        assert err <= 1e-12, f"2D engine GPU/CPU mismatch {err:.3e}"
+        cpu = {"value": n * n * xs.size * nmu / dt, "unit": "updates/s", "cores": 1,
+               "kind": "port", "cpu_model": cpu_model(),
+               "sample": f"oracle/gamma2d_ref.py (NumPy restatement of build_ptable + "
+                         f"gamma2d_entry, one thread) on {xs.size} of {nx} radial points, "
+                         f"{dt:.1f} s; GPU Γ2d on the same points: max rel gap {err:.1e}",
+               "rel_err_vs_gpu": err, "s": dt}
+    line = {"metric": "Γ2d μ-quadrature: (cell·x·μ) FP64 updates/s", "value": U / (ms / 1e3),
+            "unit": "updates/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded tables of the stated shapes)",
+            "config": {"workload": f"2D μ-quadrature engine: l_max={lmax}, p={p} -> {n} modes, "
+                                   f"Nx={nx}, {nmu} μ nodes", "updates_per_step": U,
+                       "l2_flush": "256 MiB write between timed steps (untimed)"},
+            "roofline": roof,
+            "e2e": {"value": U / e2e_s, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(n * n * 8), "s": e2e_s,
+                    "note": "the public gamma2d_matrix call with host buffers"},
+            "gpu_launches": 3, "gamma_norm": float(np.linalg.norm(g.values)),
+            "clocks": clk.summary()}
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
 def run_b200(args):
     import torch
 
@@ -645,6 +754,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "2d":
+        run_2d(args)
     elif args.config == "c3":
         run_nonsep(args)
     else:

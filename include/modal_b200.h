@@ -221,6 +221,11 @@ int mg_gamma2d(const double* q, const double* qt, const double* lw, const double
                const double* ptable, const double* mu_w, const double* wr2,
                const int64_t* modes, int p, int Nx, int L, int nmu, int n, int device,
                double* gamma);
+/* Kernel times (ms, CUDA events on the launching stream) of the calling thread's last
+ * mg_ptable / mg_gamma2d call: the P-table kernel and the cell-sum kernels.  A stage that did
+ * not run in that call (precomputed ptable) reports 0.  Measurement hook for bench.py; the
+ * reference times the same two stages with perf_counter (harness.py:369-384). */
+int mg_gamma2d_timings(double* ptable_ms, double* cells_ms);
 
 #ifdef __cplusplus
 }

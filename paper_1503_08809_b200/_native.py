@@ -57,6 +57,7 @@ _SIGS = {
                                  _vp, _vp, _vp]),
     "mg_bessel_table": (_i, [_vp, _i, _i, _i, _vp]),
     "mg_ptable": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp]),
+    "mg_gamma2d_timings": (_i, [_vp, _vp]),
     "mg_gamma2d": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp]),
     "mg_gamma_nonsep": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp,
                              _vp, _vp, _i64, _i, _vp]),

@@ -24,6 +24,8 @@ void build_qtilde_dev(const double* k, const double* wk, int Nk, const double* x
 void bessel_table(const double* z, int nz, int l_max, double* out);
 void ptable_dev(const double* q, const double* qt, const double* lw, const double* leg, int p,
                 int Nx, int L, int nmu, double* P_dev);
+void gamma2d_timings(double* ptable_ms, double* cells_ms);
+void gamma2d_reset_timings();
 void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int Nx, int nmu,
                  const double* mu_w, const double* wr2, double* gamma_host);
 
@@ -596,6 +598,7 @@ int mg_ptable(const double* q, const double* qt, const double* lw, const double*
         MG_REQUIRE(q && qt && lw && legendre && ptable, "null argument");
         MG_REQUIRE(p >= 1 && Nx >= 1 && L >= 1 && nmu >= 1, "invalid sizes");
         DeviceGuard g(device);
+        gamma2d_reset_timings();
         const size_t np = (size_t)p * p * Nx * nmu;
         DBuf<double> dP(np);
         ptable_dev(q, qt, lw, legendre, p, Nx, L, nmu, dP.p);
@@ -618,6 +621,7 @@ int mg_gamma2d(const double* q, const double* qt, const double* lw, const double
             md[3 * i] = (int)a; md[3 * i + 1] = (int)b; md[3 * i + 2] = (int)c;
         }
         DeviceGuard g(device);
+        gamma2d_reset_timings();
         const size_t np = (size_t)p * p * Nx * nmu;
         DBuf<double> dP(np);
         if (ptable)
@@ -626,6 +630,10 @@ int mg_gamma2d(const double* q, const double* qt, const double* lw, const double
             ptable_dev(q, qt, lw, legendre, p, Nx, L, nmu, dP.p);
         gamma2d_dev(dP.p, md.data(), n, p, Nx, nmu, mu_w, wr2, gamma);
     });
+}
+
+int mg_gamma2d_timings(double* ptable_ms, double* cells_ms) {
+    return guarded([&] { gamma2d_timings(ptable_ms, cells_ms); });
 }
 
 int mg_gamma_nonsep(const double* q, const double* qt, const double* C, const double* v,

@@ -18,6 +18,29 @@
 
 namespace mg {
 
+// kernel times of the calling thread's last P-table / cell-sum launch (mg_gamma2d_timings)
+thread_local double g2d_ms[2] = {0.0, 0.0};
+
+struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    EventPair() {
+        MG_CUDA(cudaEventCreate(&a));
+        MG_CUDA(cudaEventCreate(&b));
+        MG_CUDA(cudaEventRecord(a, 0));
+    }
+    double stop() {  // records the end event, waits for it, returns the elapsed ms
+        float ms = 0.f;
+        MG_CUDA(cudaEventRecord(b, 0));
+        MG_CUDA(cudaEventSynchronize(b));
+        MG_CUDA(cudaEventElapsedTime(&ms, a, b));
+        return ms;
+    }
+    ~EventPair() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
 // ---- P table -----------------------------------------------------------------------------
 // P[((a*p + b)*Nx + x)*nmu + m] as a register-tiled product over l: rows r = (a, b, x), columns
 // m, a CTA owns a 64 x 64 tile and walks l in ascending chunks of PT_BK staged through shared
@@ -368,8 +391,10 @@ void ptable_dev(const double* q, const double* qt, const double* lw, const doubl
     const int64_t R = (int64_t)p * p * Nx;
     MG_REQUIRE(ceil_div(R, PT_BM) <= 65535, "P table has too many (a, b, x) rows");
     dim3 grid(ceil_div(nmu, PT_BN), ceil_div(R, PT_BM));
+    EventPair ev;
     k_ptable_tiled<<<grid, 256>>>(dq.p, dqt.p, dlw.p, dleg.p, p, Nx, L, nmu, P_dev);
     MG_LAUNCHED();
+    g2d_ms[0] = ev.stop();
     MG_CUDA(cudaDeviceSynchronize());
 }
 
@@ -431,6 +456,7 @@ void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int N
     dw.upload(mu_w, nmu);
     dr.upload(wr2, Nx);
     dg.alloc((size_t)n * n);
+    EventPair ev;
     const bool force_lds = std::getenv("MG_G2D_LDS") != nullptr;  // A/B switch (read per call)
     if (p <= 8 && !force_lds) {
         gamma2d_dmma(P_dev, dm.p, n, p, Nx, nmu, dw.p, dr.p, dg.p);
@@ -462,8 +488,16 @@ void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int N
         k_gamma2d_reduce<<<ceil_div(cells, 256), 256>>>(dpart.p, cells, xsplit, dg.p);
         MG_LAUNCHED();
     }
+    g2d_ms[1] = ev.stop();
     MG_CUDA(cudaMemcpy(gamma_host, dg.p, (size_t)n * n * sizeof(double),
                        cudaMemcpyDeviceToHost));
 }
+
+void gamma2d_timings(double* ptable_ms, double* cells_ms) {
+    if (ptable_ms) *ptable_ms = g2d_ms[0];
+    if (cells_ms) *cells_ms = g2d_ms[1];
+}
+
+void gamma2d_reset_timings() { g2d_ms[0] = g2d_ms[1] = 0.0; }
 
 }  // namespace mg

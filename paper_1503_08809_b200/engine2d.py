@@ -24,7 +24,7 @@ from .gamma import GammaMatrix
 from .quadrature import default_mu_points, gauss_legendre, legendre_table, x_weights
 
 __all__ = ["PTable", "build_ptable", "gamma2d_matrix", "default_mu_points", "gauss_legendre",
-           "legendre_table", "DEFAULT_PTABLE_BUDGET"]
+           "legendre_table", "DEFAULT_PTABLE_BUDGET", "last_kernel_ms"]
 
 DEFAULT_PTABLE_BUDGET = 2 << 30
 
@@ -38,6 +38,15 @@ class PTable:
     @property
     def p_max(self) -> int:
         return self.values.shape[0]
+
+
+def last_kernel_ms() -> tuple:
+    """(P-table kernel ms, cell-sum kernels ms) of this thread's last build_ptable /
+    gamma2d_matrix call, from CUDA events around the launches (mg_gamma2d_timings)."""
+    import ctypes
+    a, b = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    nat.check(nat.lib().mg_gamma2d_timings(ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def _inputs(tables, legendre):
