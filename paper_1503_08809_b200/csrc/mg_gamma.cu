@@ -1272,7 +1272,20 @@ static void run_pipeline(mg_plan* P, const std::vector<MgRow>& hrows,
         const int nb = (int)(B.e1 - B.b1);
         const int tf = tile_first[B.bidx], tl = tile_first[B.bidx + 1];
         MG_NVTX("mg:batch_enqueue");
-#if MG_SIDE
+#if MG_SIDE == 3
+        // panels of batch k alone on the main stream, then the pair products of batch k on the
+        // side stream (it waits for the panels, which follow x(k-1) on the main stream, so S
+        // has been consumed): they become runnable together with the run contraction, whose
+        // higher-priority CTAs are placed first
+        prof_mark(P, 0, ms);
+        issue_panels(k, ms);
+        MG_CUDA(cudaEventRecord(P->ev_panel[0], ms));
+        MG_CUDA(cudaStreamWaitEvent(ss, P->ev_panel[0], 0));
+        prof_side(P, ss, true);
+        issue_pairs(k, ss);
+        prof_side(P, ss, false);
+        MG_CUDA(cudaEventRecord(P->ev_s, ss));
+#elif MG_SIDE
         // side stream, once x(k-1) has consumed S: pair products of batch k (and, MG_SIDE 2,
         // the panels of batch k), beside the run contraction of batch k
         if (k > 0) MG_CUDA(cudaStreamWaitEvent(ss, P->ev_x, 0));

@@ -364,6 +364,44 @@ class TestGamma2D:
         assert gap_rel(got, want) < 1e-12
         assert np.array_equal(gamma2d_matrix(t, m, r, rule, leg, ptable=pt).values, got)
 
+    @pytest.mark.parametrize("lds", [False, True])
+    def test_custom_mode_subset(self, lds, monkeypatch):
+        """A mapping that is not the default k-major list (repeated indices, gaps, arbitrary
+        order) through both cell kernels."""
+        from oracle import gamma2d_ref
+        from paper_1503_08809_b200 import gamma2d_matrix, gauss_legendre, legendre_table
+        if lds:
+            monkeypatch.setenv("MG_G2D_LDS", "1")
+        else:
+            monkeypatch.delenv("MG_G2D_LDS", raising=False)
+        t, r = TestEdgeCases().random_tables(2, 28, 6, 17, seed=5)
+        entries = np.array([[5, 5, 5], [0, 0, 0], [0, 2, 4], [1, 1, 3], [0, 1, 2], [2, 3, 5],
+                            [3, 3, 4]])
+        m = ModeMapping(entries, 6)
+        rule = gauss_legendre(45)
+        leg = legendre_table(28, rule)
+        P = gamma2d_ref.ptable(t.q, t.q_tilde, t.C, t.v, 2, 28, leg)
+        want = gamma2d_ref.gamma2d(P, entries, rule.weights, x_weights(r.r))
+        got = gamma2d_matrix(t, m, r, rule, leg).values
+        assert got.shape == (7, 7)
+        assert gap_rel(got, want) < 1e-12
+
+    def test_kernel_timings_hook(self, g_desk):
+        from paper_1503_08809_b200 import build_ptable, gamma2d_matrix, gauss_legendre, legendre_table
+        from paper_1503_08809_b200.engine2d import last_kernel_ms
+        t, m, r = desk_problem(g_desk, "desk")
+        rule = gauss_legendre(27)
+        leg = legendre_table(t.l_max, rule)
+        gamma2d_matrix(t, m, r, rule, leg)
+        a, b = last_kernel_ms()
+        assert a > 0 and b > 0
+        pt = build_ptable(t, r, rule, leg)
+        a, b = last_kernel_ms()
+        assert a > 0 and b == 0
+        gamma2d_matrix(t, m, r, rule, leg, ptable=pt)
+        a, b = last_kernel_ms()
+        assert a == 0 and b > 0
+
     def test_budget_and_errors(self, g_desk):
         from paper_1503_08809_b200 import build_ptable, gauss_legendre, legendre_table
         t, m, r = desk_problem(g_desk, "desk")
