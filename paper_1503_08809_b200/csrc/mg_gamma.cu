@@ -363,10 +363,11 @@ constexpr int PP_CHUNK = 16;  // pairs per block of the pair-product kernel
 #ifndef MG_PP_UNROLL
 #define MG_PP_UNROLL 2
 #endif
-// 128 threads x <= 32 registers: one warp per SM sub-partition, 1024 registers each (the
-// smallest footprint; with the 13-warp x 128-register run contraction no side CTA fits on
-// its fullest sub-partition, so the side stream mostly fills the contractions' tails —
-// capping the run contraction at 120 registers to make room was measured slower).
+// 128 threads x <= 32 registers: one warp per SM sub-partition, 1024 registers each.  Beside
+// the 13-warp x 128-register run contraction no side CTA of any size is placed (registers are
+// allocated per CTA in units of 4 warps, so 13 warps take the whole file: tools/coresidency.cu,
+// profiles/r02_coresidency.txt), so the side stream fills the contractions' tails — capping
+// the run contraction at 120 registers to make room was measured slower.
 __global__ void __maxnreg__(MG_PP_MAXREG)
 k_pair_products(const MgRow* __restrict__ rows, int row_b1, const double* __restrict__ QT,
                 int p, int P2, int NxP, int l_min, double* __restrict__ S, MgBounds bd) {
