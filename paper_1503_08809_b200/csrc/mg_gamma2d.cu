@@ -223,7 +223,7 @@ __global__ void k_gamma2d_reduce(const double* __restrict__ partial, int64_t cel
     gamma[i] = acc / (48.0 * 3.141592653589793);
 }
 
-// ---- Γ cells on the FP64 tensor pipe (p ≤ 8) -------------------------------------------------
+// ---- Γ cells on the FP64 tensor pipe (p ≤ 24) ------------------------------------------------
 // The permanent splits along its last row:  perm = Σ_k P[r2,c_k] · V[(r0,r1)][(c_i,c_j)]  with
 // V[(a,b)][(c,d)] = P[a,c]P[b,d] + P[a,d]P[b,c]  ((i,j) the two columns other than k), so with
 // the sample index s = (x, μ) and W_s = w_x r_x² w_μ
@@ -231,10 +231,12 @@ __global__ void k_gamma2d_reduce(const double* __restrict__ partial, int64_t cel
 // is one GEMM — M = p² rows, N = (p(p+1)/2)² columns, K = Nx·n_μ — and every cell is three
 // entries of D.  It costs about as many FLOPs as the per-cell form (p⁶/2 against 10·p⁶/36 FP64
 // instructions per sample) but runs them as DMMA.8x8x4 with ~0.9 shared-memory reads per DMMA
-// instead of ten per cell-sample, which is what bounded k_gamma2d_cells.  A CTA (8 warps) owns
-// 24 n-fragments and a contiguous range of samples (split-K, partials reduced in order by
-// k_gamma2d_gather); P_s chunks of 64 samples are double-buffered through shared memory with
-// 8-byte cp.async; the B operand is never stored: a lane forms its element from four P reads.
+// instead of ten per cell-sample, which is what bounded k_gamma2d_cells.  A CTA owns 24-32
+// n-fragments, one M tile of up to 64 rows (p > 8: several M tiles, grid.z) and a contiguous
+// range of samples (split-K, partials reduced in order by k_gamma2d_gather); chunks of all p²
+// rows of P_s are double-buffered through shared memory with 8-byte cp.async (128 samples per
+// chunk at p <= 8, 64 / 32 / 16 as p² grows); the B operand is never stored: a lane forms its
+// element from four P reads.
 // Tile: WARPS warps of FN n-fragments each, KC samples per stage, row stride KC + 4 (fragment
 // reads of (row g, sample t) are then bank-conflict free).  Measured (profiles/r02_2d_engine.txt):
 // 12 warps x 2 fragments x 128 samples is fastest at p = 7, 8 (7-8 m-fragments feed 14-16 DMMAs
@@ -251,11 +253,14 @@ template <int MF, int G2D_WARPS, int G2D_FN, int G2D_KC>
 __global__ void __launch_bounds__(G2D_WARPS * 32, 1)
 k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
                const double* __restrict__ mu_w, int p, int nmu, int64_t S, int nchunks,
-               int N, int Npad, double* __restrict__ Dpart) {
+               int N, int Npad, int srows, double* __restrict__ Dpart) {
+    // srows = p² rounded up to whole M tiles of MF*8 rows: every CTA stages all p² rows of P
+    // (the B operand pairs any two of them); its A rows are M tile blockIdx.z of those
     extern __shared__ double sm[];
-    constexpr int ROWS = MF * 8, G2D_LD = G2D_KC + 4;
-    double* Ps = sm;                               // [2][ROWS][G2D_LD]
-    double* Ws = sm + 2 * ROWS * G2D_LD;           // [2][G2D_KC]
+    constexpr int G2D_LD = G2D_KC + 4;
+    double* Ps = sm;                               // [2][srows][G2D_LD]
+    double* Ws = sm + 2 * srows * G2D_LD;          // [2][G2D_KC]
+    const int arow0 = blockIdx.z * MF * 8;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int pp = p * p, P2 = p * (p + 1) / 2;
     // this lane's B columns: n = (a'<=b', c'<=d') -> four row offsets into the staged P block
@@ -280,9 +285,9 @@ k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
     // sample chunks of this CTA
     const int c0 = (int)((int64_t)nchunks * blockIdx.y / gridDim.y);
     const int c1 = (int)((int64_t)nchunks * (blockIdx.y + 1) / gridDim.y);
-    // padding rows (pp <= row < ROWS) stay zero in both buffers
-    for (int e = tid; e < 2 * ROWS * G2D_LD; e += blockDim.x)
-        if ((e / G2D_LD) % ROWS >= pp) Ps[e] = 0.0;
+    // padding rows (pp <= row < srows) stay zero in both buffers
+    for (int e = tid; e < 2 * srows * G2D_LD; e += blockDim.x)
+        if ((e / G2D_LD) % srows >= pp) Ps[e] = 0.0;
 
     // staging: a thread copies one sample column k of rows kr, kr + RSTEP, ... (8-byte cp.async,
     // zero-filled past the last sample), so a chunk costs it one copy and two adds per element
@@ -293,7 +298,7 @@ k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
         const int64_t sidx = (int64_t)ch * G2D_KC + kcol;
         const bool ok = sidx < S;
         const double* src = ok ? P + (int64_t)kr * S + sidx : P;
-        double* dst = Ps + buf * ROWS * G2D_LD + kr * G2D_LD + kcol;
+        double* dst = Ps + buf * srows * G2D_LD + kr * G2D_LD + kcol;
         const int64_t sstep = ok ? (int64_t)RSTEP * S : 0;
         const int bytes = ok ? 8 : 0;
         for (int row = kr; row < pp; row += RSTEP) {
@@ -322,7 +327,8 @@ k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
         }
         __syncthreads();
         if (warp_live) {
-            const double* ps = Ps + buf * ROWS * G2D_LD;
+            const double* ps = Ps + buf * srows * G2D_LD;
+            const double* pa = ps + (arow0 + g) * G2D_LD;
             const double* ws = Ws + buf * G2D_KC;
 #pragma unroll 4
             for (int k = t; k < G2D_KC; k += 4) {
@@ -334,7 +340,7 @@ k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
                                           ps[o[f][2] + k] * ps[o[f][3] + k]);
 #pragma unroll
                 for (int m = 0; m < MF; ++m) {
-                    const double a = ps[(m * 8 + g) * G2D_LD + k];
+                    const double a = pa[m * 8 * G2D_LD + k];
 #pragma unroll
                     for (int f = 0; f < G2D_FN; ++f) dmma884(acc[m][f], a, b[f]);
                 }
@@ -343,7 +349,7 @@ k_gamma2d_dmma(const double* __restrict__ P, const double* __restrict__ wr2,
         __syncthreads();  // the next iteration's stage() overwrites the other buffer
     }
     if (!warp_live) return;
-    double* out = Dpart + (int64_t)blockIdx.y * ROWS * Npad;
+    double* out = Dpart + ((int64_t)blockIdx.y * srows + arow0) * Npad;
 #pragma unroll
     for (int m = 0; m < MF; ++m)
 #pragma unroll
@@ -408,43 +414,70 @@ int gamma2d_xsplit(int n, int Nx) {
     return (int)std::max<int64_t>(1, xs);
 }
 
+// Shared memory of one CTA: two staged blocks of srows x (KC + 4) doubles plus the weights.
+static size_t g2d_smem(int srows, int kc) {
+    return ((size_t)2 * srows * (kc + 4) + 2 * kc) * sizeof(double);
+}
+constexpr size_t G2D_SMEM_CAP = 200 * 1024;
+constexpr size_t G2D_PART_CAP = size_t(1) << 30;  // split-K partials of D
+
 template <int MF, int WARPS, int FN, int KC>
 static void launch_gamma2d_dmma(const double* P_dev, const int* modes_dev, int n, int p, int Nx,
                                 int nmu, const double* mu_w_dev, const double* wr2_dev,
                                 double* gamma_dev) {
     const int P2 = p * (p + 1) / 2, N = P2 * P2, Npad = (int)round_up(N, 8);
-    constexpr int rows = MF * 8, LD = KC + 4;
+    const int mtiles = ceil_div(p * p, MF * 8), srows = mtiles * MF * 8;
     const int64_t S = (int64_t)Nx * nmu;
     const int nchunks = ceil_div(S, KC);
     const int gx = ceil_div(Npad / 8, FN * WARPS);
-    // one CTA per SM in total, at least 4 chunks per CTA
-    const int ksplit = std::max(1, std::min(std::max(148 / gx, 1), std::max(nchunks / 4, 1)));
-    DBuf<double> dpart((size_t)ksplit * rows * Npad);
-    const size_t shm = ((size_t)2 * rows * LD + 2 * KC) * sizeof(double);
+    // about one CTA per SM in total, at least 4 chunks per CTA, partials within their cap
+    int ksplit = std::max(1, std::min(std::max(148 / (gx * mtiles), 1), std::max(nchunks / 4, 1)));
+    ksplit = (int)std::max<size_t>(
+        1, std::min<size_t>(ksplit, G2D_PART_CAP / ((size_t)srows * Npad * sizeof(double))));
+    DBuf<double> dpart((size_t)ksplit * srows * Npad);
+    const size_t shm = g2d_smem(srows, KC);
     MG_CUDA(cudaFuncSetAttribute(k_gamma2d_dmma<MF, WARPS, FN, KC>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_gamma2d_dmma<MF, WARPS, FN, KC><<<dim3(gx, ksplit), WARPS * 32, shm>>>(
-        P_dev, wr2_dev, mu_w_dev, p, nmu, S, nchunks, N, Npad, dpart.p);
+    k_gamma2d_dmma<MF, WARPS, FN, KC><<<dim3(gx, ksplit, mtiles), WARPS * 32, shm>>>(
+        P_dev, wr2_dev, mu_w_dev, p, nmu, S, nchunks, N, Npad, srows, dpart.p);
     MG_LAUNCHED();
     const int64_t cells = (int64_t)n * n;
-    k_gamma2d_gather<<<ceil_div(cells, 256), 256>>>(dpart.p, ksplit, rows, Npad, modes_dev, n, p,
+    k_gamma2d_gather<<<ceil_div(cells, 256), 256>>>(dpart.p, ksplit, srows, Npad, modes_dev, n, p,
                                                       gamma_dev);
     MG_LAUNCHED();
 }
 
+// The DMMA form serves a basis if its staged P block fits shared memory with at least 16
+// samples per chunk and one set of D partials fits the cap (p <= 24 with these caps); larger
+// bases use the per-cell kernel.
+static bool gamma2d_dmma_fits(int p) {
+    if (p <= 8) return true;
+    const int srows = (int)round_up(p * p, 64), P2 = p * (p + 1) / 2;
+    return g2d_smem(srows, 16) <= G2D_SMEM_CAP &&
+           (size_t)srows * round_up((int64_t)P2 * P2, 8) * sizeof(double) <= G2D_PART_CAP;
+}
+
 static void gamma2d_dmma(const double* P_dev, const int* modes_dev, int n, int p, int Nx, int nmu,
                          const double* mu_w_dev, const double* wr2_dev, double* gamma_dev) {
-#define MG_G2D_CASE(MF, W)                                                                    \
-    case MF:                                                                                  \
-        launch_gamma2d_dmma<MF, W, 2, 128>(P_dev, modes_dev, n, p, Nx, nmu, mu_w_dev, wr2_dev, \
-                                           gamma_dev);                                        \
-        break;
-    switch (ceil_div(p * p, 8)) {  // m-fragments: p = 1..8 -> 1, 1, 2, 2, 4, 5, 7, 8
-        MG_G2D_CASE(1, 16) MG_G2D_CASE(2, 16) MG_G2D_CASE(4, 16) MG_G2D_CASE(5, 16)
-        MG_G2D_CASE(7, 12) MG_G2D_CASE(8, 12)
-        default: fail(MG_EINVAL, "gamma2d_dmma: p must be <= 8");
+#define MG_G2D_GO(MF, W, KC)                                                                   \
+    launch_gamma2d_dmma<MF, W, 2, KC>(P_dev, modes_dev, n, p, Nx, nmu, mu_w_dev, wr2_dev,      \
+                                      gamma_dev)
+    if (p > 8) {  // several M tiles of 64 rows; the chunk length is what shared memory allows
+        const int srows = (int)round_up(p * p, 64);
+        if (g2d_smem(srows, 64) <= G2D_SMEM_CAP) MG_G2D_GO(8, 12, 64);
+        else if (g2d_smem(srows, 32) <= G2D_SMEM_CAP) MG_G2D_GO(8, 12, 32);
+        else MG_G2D_GO(8, 12, 16);
+        return;
     }
-#undef MG_G2D_CASE
+    switch (ceil_div(p * p, 8)) {  // m-fragments: p = 1..8 -> 1, 1, 2, 2, 4, 5, 7, 8
+        case 1: MG_G2D_GO(1, 16, 128); break;
+        case 2: MG_G2D_GO(2, 16, 128); break;
+        case 4: MG_G2D_GO(4, 16, 128); break;
+        case 5: MG_G2D_GO(5, 16, 128); break;
+        case 7: MG_G2D_GO(7, 12, 128); break;
+        default: MG_G2D_GO(8, 12, 128); break;
+    }
+#undef MG_G2D_GO
 }
 
 void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int Nx, int nmu,
@@ -458,7 +491,7 @@ void gamma2d_dev(const double* P_dev, const int* modes_host, int n, int p, int N
     dg.alloc((size_t)n * n);
     EventPair ev;
     const bool force_lds = std::getenv("MG_G2D_LDS") != nullptr;  // A/B switch (read per call)
-    if (p <= 8 && !force_lds) {
+    if (!force_lds && gamma2d_dmma_fits(p)) {
         gamma2d_dmma(P_dev, dm.p, n, p, Nx, nmu, dw.p, dr.p, dg.p);
     } else {
         const int xsplit = gamma2d_xsplit(n, Nx);

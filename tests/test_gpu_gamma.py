@@ -336,14 +336,18 @@ class TestGamma2D:
                                                      (3, 34, 7, 19, 65),     # 33 = 32 + 1 rows of l
                                                      (2, 150, 3, 130, 228),  # 19 row tiles
                                                      (2, 30, 8, 23, 50),     # p = 8: 8 m-fragments
-                                                     (2, 24, 9, 11, 40),     # p > 8: per-cell form
+                                                     (2, 24, 9, 11, 40),     # p > 8: 2 M tiles
+                                                     (2, 20, 12, 7, 30),     # 3 M tiles, 64-sample chunks
+                                                     (2, 18, 15, 5, 24),     # 4 M tiles, 32-sample chunks
+                                                     (2, 14, 20, 3, 20),     # 7 M tiles, 16-sample chunks
+                                                     (2, 12, 25, 2, 12),     # beyond the DMMA form
                                                      (2, 12, 1, 5, 20),      # one mode
                                                      (2, 40, 2, 9, 64)])
     def test_tiled_kernels_vs_oracle(self, lmin, lmax, p, nx, nmu, lds, monkeypatch):
         """Sizes that cross every tile edge of the P-table kernel (64 x 64 x 32: partial row,
         column and l tiles) and of both cell kernels — the DMMA form (p <= 8: partial
-        m-fragments, partial n-fragments, idle warps, split-K with a short last chunk) and the
-        per-cell form (MG_G2D_LDS=1 or p > 8: x chunks per CTA, μ chunks of 64, partial 16 x 16
+        m-fragments, partial n-fragments, idle warps, split-K with a short last chunk,
+        several M tiles for p > 8) and the per-cell form (MG_G2D_LDS=1 or p > 24: x chunks per CTA, μ chunks of 64, partial 16 x 16
         cell tiles) — against oracle/gamma2d_ref.py (pinned to the reference's tables)."""
         from oracle import gamma2d_ref
         if lds:
