@@ -552,14 +552,19 @@ def run_b200(args):
     exec_flops = sum(fams.values())
     step_s = ms / 1e3
     traffic, traffic_note = None, None
-    tfile = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
-    if os.path.exists(tfile):
-        tr = json.load(open(tfile)).get(names[dom])
+    for rnd in ("r02", "r01"):                       # newest committed ncu --set full capture
+        tfile = os.path.join(ROOT, "profiles", f"{rnd}_ncu_traffic.json")
+        if not os.path.exists(tfile):
+            continue
+        table = json.load(open(tfile))
+        tr = next((v for k, v in table.items() if k.startswith(names[dom])), None)
         if tr:
             traffic = tr["dram_bytes"]
             traffic_note = (f"dram read+write bytes of one profiled {names[dom]} launch "
                             f"({tr['duration_ms']:.2f} ms, config-1 l2 slab [1400,1420)) from "
-                            f"ncu --set full, profiles/r01_ncu_full_c1.txt")
+                            f"ncu --set full, profiles/{rnd}_ncu_full_c1.txt: the H/S "
+                            f"intermediates' round trip (DESIGN.md §4), not re-reads of q̃")
+            break
     line = {
         "metric": "Γ projection: (l-triple·x·mode) FP64 updates/s",
         "value": U / step_s,
