@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from .engine3d import _base_meta
+from .engine3d import _FP_POOL, _meta_dict
 from .gamma import GammaMatrix
 from .quadrature import default_mu_points, gauss_legendre, legendre_table, x_weights
 
@@ -86,6 +86,8 @@ def gamma2d_matrix(tables, mapping, grid, rule, legendre, integrator: str = "tra
         raise ValueError(f"radial grid has {wr2.size} points but q_tilde has {nr} (n_radial)")
     muw = np.ascontiguousarray(rule.weights, np.float64)
     out = np.zeros((n, n))
+    fp = _FP_POOL.submit(lambda: (tables.fingerprint(), grid.fingerprint(),
+                                  mapping.fingerprint()))   # overlaps the GPU call
     if ptable is not None:
         pv = np.ascontiguousarray(ptable.values, np.float64)
         if pv.shape != (p, p, nr, nmu):
@@ -102,7 +104,7 @@ def gamma2d_matrix(tables, mapping, grid, rule, legendre, integrator: str = "tra
         nat.check(nat.lib().mg_gamma2d(nat.ptr(q), nat.ptr(qt), nat.ptr(lw), nat.ptr(leg),
                                        None, nat.ptr(muw), nat.ptr(wr2), nat.ptr(e), p, nr,
                                        lw.size, nmu, n, int(device), nat.ptr(out)))
-    meta = _base_meta(tables, grid, mapping, integrator, "n/a", 1, workers)
+    meta = _meta_dict(tables, grid, mapping, integrator, "n/a", 1, workers, *fp.result())
     meta.pop("h2_mode"), meta.pop("block")
     meta.update({"engine": "modal2d", "n_mu": nmu, "workers": workers})
     return GammaMatrix(out, meta)
