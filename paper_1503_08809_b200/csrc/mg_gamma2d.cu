@@ -430,8 +430,13 @@ static void launch_gamma2d_dmma(const double* P_dev, const int* modes_dev, int n
     const int64_t S = (int64_t)Nx * nmu;
     const int nchunks = ceil_div(S, KC);
     const int gx = ceil_div(Npad / 8, FN * WARPS);
-    // about one CTA per SM in total, at least 4 chunks per CTA, partials within their cap
-    int ksplit = std::max(1, std::min(std::max(148 / (gx * mtiles), 1), std::max(nchunks / 4, 1)));
+    // split-K: one CTA per SM in total when the (N tile, M tile) grid divides the machine well
+    // (at least 85 % of the SMs busy); otherwise about six waves of CTAs (one resident per SM), so the last, partly
+    // filled wave costs little; at least 4 chunks per CTA, partials within their cap
+    const int tiles = gx * mtiles;
+    int ksplit = tiles <= 148 ? 148 / tiles : 0;
+    if (ksplit * tiles * 100 < 85 * 148) ksplit = ceil_div(6 * 148, tiles);  // < 85 % of one wave
+    ksplit = std::max(1, std::min(ksplit, std::max(nchunks / 4, 1)));
     ksplit = (int)std::max<size_t>(
         1, std::min<size_t>(ksplit, G2D_PART_CAP / ((size_t)srows * Npad * sizeof(double))));
     DBuf<double> dpart((size_t)ksplit * srows * Npad);
