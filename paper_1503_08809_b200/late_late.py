@@ -13,15 +13,16 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as nat
-from .engine3d import _base_meta, gamma3d_matrix
+from .engine3d import _meta_dict, gamma3d_matrix
 from .gamma import GammaMatrix
 
 __all__ = ["gamma_late_late", "gamma_estimator"]
 
 
 def gamma_late_late(tables, mapping, h2_mode: str = "gosper", *,
-                    device: int = 0) -> GammaMatrix:
-    """⟨Q_n, Q_m⟩ on the tetrahedral domain, [n, n] symmetric."""
+                    device: int = 0, _fingerprints=None) -> GammaMatrix:
+    """⟨Q_n, Q_m⟩ on the tetrahedral domain, [n, n] symmetric.  `_fingerprints` = (tables,
+    mapping) digests already computed by the caller (gamma_estimator hashes the tables once)."""
     if h2_mode not in nat.MG_H2:
         raise ValueError(f"unknown h2_mode {h2_mode!r}")
     q = np.ascontiguousarray(tables.q, np.float64)
@@ -37,9 +38,9 @@ def gamma_late_late(tables, mapping, h2_mode: str = "gosper", *,
         nat.ptr(q), nat.ptr(qt), nat.ptr(C), nat.ptr(v), nat.ptr(wr2), nat.ptr(e), q.shape[0],
         1, n, int(tables.l_min), int(tables.l_max), nat.MG_H2[h2_mode], 0, -1, 1,
         nat.ptr(devs), nat.ptr(out)))
+    ft, fm = _fingerprints or (tables.fingerprint(), mapping.fingerprint())
     meta = {"engine": "modal3d-QQ", "l_min": tables.l_min, "l_max": tables.l_max,
-            "p_max": tables.p_max, "n_max": n, "h2_mode": h2_mode,
-            "tables": tables.fingerprint(), "mapping": mapping.fingerprint()}
+            "p_max": tables.p_max, "n_max": n, "h2_mode": h2_mode, "tables": ft, "mapping": fm}
     return GammaMatrix(out, meta)
 
 
@@ -48,8 +49,9 @@ def gamma_estimator(tables, mapping, grid, h2_mode: str = "gosper",
     """(Γ, ⟨Q,Q⟩, Γ') with Γ = ⟨Q,Q⟩⁻¹ Γ' (PAPER.md:718-722); Γ' = gamma3d_matrix."""
     gp = gamma3d_matrix(tables, mapping, grid, h2_mode=h2_mode, integrator=integrator,
                         device=device)
-    qq = gamma_late_late(tables, mapping, h2_mode, device=device)
+    ft, fg, fm = gp.meta["tables"], gp.meta["grid"], gp.meta["mapping"]
+    qq = gamma_late_late(tables, mapping, h2_mode, device=device, _fingerprints=(ft, fm))
     full = np.linalg.solve(qq.values, gp.values)
-    meta = _base_meta(tables, grid, mapping, integrator, h2_mode, 1, 1)
+    meta = _meta_dict(tables, grid, mapping, integrator, h2_mode, 1, 1, ft, fg, fm)
     meta["engine"] = "modal3d-estimator"
     return GammaMatrix(full, meta), qq, gp
