@@ -16,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as nat
-from .engine3d import _base_meta, check_shapes
+from .engine3d import _FP_POOL, _meta_dict, check_shapes
 from .gamma import GammaMatrix
 from .quadrature import x_weights
 from .scheduler import slab_plan
@@ -77,6 +77,8 @@ def gamma3d_matrix_distributed(tables, mapping, grid, h2_mode="gosper", integrat
         raise ValueError(f"unknown h2_mode {h2_mode!r}")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     wr2 = x_weights(grid.r, integrator)
+    fp = _FP_POOL.submit(lambda: (tables.fingerprint(), grid.fingerprint(),
+                                  mapping.fingerprint()))   # hashed beside the slab's GPU work
     a, b = rank_slab(int(tables.l_min), int(tables.l_max), tables.p_max, wr2.size, rank, world)
     if partial_fn is None:
         import os
@@ -101,6 +103,6 @@ def gamma3d_matrix_distributed(tables, mapping, grid, h2_mode="gosper", integrat
         t = torch.from_numpy(np.ascontiguousarray(partial_fn(tables, mapping, wr2, a, b,
                                                              h2_mode)))
     merged = merge_rank_partials(t, group).cpu().numpy()
-    meta = _base_meta(tables, grid, mapping, integrator, h2_mode, block, workers)
+    meta = _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers, *fp.result())
     meta["ranks"] = world
     return GammaMatrix(merged, meta)

@@ -121,13 +121,9 @@ def check_shapes(q, qt, C, v, wr2, l_min: int, l_max: int) -> None:
                          f"{qt.shape[1]} (n_radial)")
 
 
-def _base_meta(tables, grid, mapping, integrator, h2_mode, block, workers):
-    """Provenance keys of engine3d.py:139-153,172-174."""
-    return _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers,
-                      tables.fingerprint(), grid.fingerprint(), mapping.fingerprint())
-
-
 def _meta_dict(tables, grid, mapping, integrator, h2_mode, block, workers, ft, fg, fm):
+    """Provenance keys of engine3d.py:139-153,172-174; ft/fg/fm = the tables / grid / mapping
+    fingerprints (hashed on the `_FP_POOL` thread beside the GPU call by every drop-in)."""
     return {
         "engine": "modal3d",
         "l_min": tables.l_min,
