@@ -69,7 +69,7 @@ def build_ptable(tables, grid, rule, legendre, budget_bytes: int = DEFAULT_PTABL
     q, qt, lw, leg = _inputs(tables, legendre)
     if np.size(grid.r) != nr:
         raise ValueError(f"radial grid has {np.size(grid.r)} points but q_tilde has {nr}")
-    out = np.zeros((p, p, nr, nmu))
+    out = np.empty((p, p, nr, nmu))      # every element is written by the device copy
     nat.check(nat.lib().mg_ptable(nat.ptr(q), nat.ptr(qt), nat.ptr(lw), nat.ptr(leg), p, nr,
                                   lw.size, nmu, int(device), nat.ptr(out)))
     return PTable(out)
